@@ -1,0 +1,83 @@
+"""CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` / ``--impl reference``
+legs may import this package.  The product package ``paper_2001_01473_b200`` never imports it and
+shares no code with it (the only shared module is ``inputs``, which holds no stencil arithmetic).
+
+Contents
+  * :func:`run` -- the plain double-buffered time loop of PAPER.md fig:jacobi2d with
+    Table 2's stencil definitions, in C (oracle.c, OpenMP over the outer dimension),
+    fp32 or fp64 arithmetic as the run.
+  * :mod:`oracle.geometry` -- the paper's blocking bookkeeping formulas
+    written out independently of the library's C++ (bit-exact checks of an5d_describe /
+    an5d_schedule).
+  * :mod:`oracle.model` -- the paper's section-5 performance model in "V100 mode".
+
+Pins (tests/test_oracle_pins.py) tie this oracle to values fixed by the paper and mathematics:
+constant field, linear field, quadratic closed form, mirrored impulse, T-fold self-convolution,
+brute force on tiny grids.  See DESIGN.md "Oracle and pins".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile oracle.c with gcc (-O2 -ffp-contract=off -fopenmp): IEEE mul/add, no FMA contraction."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+                               "-shared", _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        lib = ctypes.CDLL(_LIB)
+        for name, ct in (("oracle_run_f32", ctypes.c_float), ("oracle_run_f64", ctypes.c_double)):
+            fn = getattr(lib, name)
+            fn.restype = ctypes.c_int
+            fn.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                           ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_int64, ctypes.c_int]
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def max_threads() -> int:
+    return _load().oracle_max_threads()
+
+
+def run(grid: np.ndarray, rad: int, shape: int, coeffs, divisor: float, T: int, dtype=np.float32,
+        nthreads: int = 0) -> np.ndarray:
+    """T steps of the naive double-buffered loop on a dense grid (ring included); returns a new array.
+
+    ``coeffs`` is the dense (2r+1)^ndim table (index order outer..x; entry d multiplies the
+    neighbour at offset +d), rounded once to ``dtype``; ``divisor`` divides the sum (IEEE division)
+    when != 1.  ``nthreads`` <= 0 uses all OpenMP threads.
+    """
+    lib = _load()
+    g = np.ascontiguousarray(grid, dtype=dtype)
+    out = np.empty_like(g)
+    ext = (ctypes.c_int64 * g.ndim)(*g.shape)
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64).reshape(-1))
+    fn = lib.oracle_run_f32 if g.dtype == np.float32 else lib.oracle_run_f64
+    nt = nthreads if nthreads > 0 else lib.oracle_max_threads()
+    rc = fn(g.ndim, int(rad), int(shape), c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(divisor), ext,
+            g.ctypes.data, out.ctypes.data, int(T), int(nt))
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return out
