@@ -1,0 +1,159 @@
+/*
+ * an5d.h -- C ABI of the B200-native N.5D temporally blocked stencil library (libAN5D).
+ *
+ * Method: AN5D, Matsumura et al., arXiv 2001.01473 ("PAPER.md" below, cited P:<line>).
+ *   - Problem: a double-buffered grid A[2] with a constant (Dirichlet) boundary ring, updated by a
+ *     star or box stencil of radius rad with constant coefficients for I_T time steps
+ *     (fig:jacobi2d P:400-418, Table 2).
+ *   - Method: N.5D blocking = overlapped-tile temporal blocking (halo b_T*rad per side, recomputed
+ *     redundantly) on top of (N-1)-D spatial blocking that streams along the outermost
+ *     dimension, with the streaming dimension divided into stream blocks
+ *      and box stencils computed by associative partial sums.
+ *   - Host loop of sweeps, each advancing up to b_T steps, with a final-block adjustment.
+ *
+ * Conventions (all functions):
+ *   - Layout: row-major, innermost dimension x contiguous.  The STREAMING dimension is the
+ *     OUTERMOST array dimension (y in 2D, z in 3D): "the loop after the time loop represents the
+ *     streaming dimension".  `extents` are given outermost first and INCLUDE the rad-wide
+ *     boundary ring on every face: extent_i = I_S_i + 2*rad.
+ *   - `pitches` (may be NULL = dense): element strides of the ndim-1 outer dimensions, outermost
+ *     first (2D: {row stride}; 3D: {plane stride, row stride}).
+ *   - Alignment (B200 128-bit vector path): the address of element x = rad of every row must be
+ *     16-byte aligned, i.e. (base + rad*elem_size) % 16 == 0 and every pitch*elem_size % 16 == 0.
+ *     Violations return AN5D_ERR_UNSUPPORTED before any launch (the Python binding allocates
+ *     compliant views: paper_2001_01473_b200.empty_grid).
+ *   - Pointers named grid_* are DEVICE pointers owned by the caller; the library retains none of
+ *     them after a call returns and performs no hidden device allocation.
+ *   - Streams: every launch goes to `cuda_stream` (a cudaStream_t; NULL = legacy default stream)
+ *     and is asynchronous.  Argument/feasibility errors are detected before any launch, so an
+ *     error return means nothing was written.  CUDA launch errors surface as AN5D_ERR_CUDA.
+ *   - No C++ exception crosses this ABI.  an5d_last_error() returns a thread-local message.
+ *   - Threading: a plan may be used from one thread at a time; distinct plans are independent.
+ */
+#ifndef AN5D_H
+#define AN5D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AN5D_OK = 0,
+    AN5D_ERR_INVALID_ARGUMENT = 1,   /* null pointer, bad ndim/radius/shape/dtype, T < 0, ...   */
+    AN5D_ERR_INFEASIBLE_CONFIG = 2,  /* empty compute region b_S - 2*b_T*rad < 1         */
+    AN5D_ERR_BLOCK_TOO_LARGE = 3,    /* tile does not fit the kernel instance / thread limits    */
+    AN5D_ERR_SHAPE_MISMATCH = 4,     /* extents smaller than 2*rad+1, coefficient count wrong,   */
+                                     /* STAR table with a non-zero off-axis entry               */
+    AN5D_ERR_UNSUPPORTED = 5,        /* no kernel instance for (ndim,rad,shape,dtype,b_T,vec),   */
+                                     /* or misaligned base/pitch for the vector path            */
+    AN5D_ERR_CUDA = 6,               /* a CUDA runtime error (message in an5d_last_error)       */
+    AN5D_ERR_OUT_OF_MEMORY = 7
+} an5d_status;
+
+typedef enum { AN5D_STAR = 0, AN5D_BOX = 1 } an5d_shape;
+typedef enum { AN5D_F32 = 0, AN5D_F64 = 1 } an5d_dtype;   /* single and double */
+
+typedef struct an5d_plan an5d_plan; /* opaque */
+
+/* Blocking configuration (P:516-519 compile-time parameters of the paper; run-time here).
+ * Any field set to 0 is chosen by the host planner (an5d_plan_config).                        */
+typedef struct {
+    int bT;          /* temporal blocking degree b_T of a full sweep                      */
+    int bS[2];       /* logical spatial tile b_S_i INCLUDING the 2*b_T*rad halo, blocked dims     */
+                     /* only: 2D {b_S_x, 0}; 3D {b_S_y, b_S_x}.  The kernel loads   */
+                     /* b_S_x rounded up so that halos are whole 16-byte vectors.    */
+    int64_t h;       /* stream-block length h_SN along the streaming dimension       */
+    int vec;         /* cells per thread along y (3D) or x (2D): register tiling factor V        */
+} an5d_config;
+
+/* Bookkeeping of one sweep of degree bT under `cfg` (bit-exact).        */
+typedef struct {
+    int ndim, rad, bT;
+    int64_t interior[3];        /* I_S_i, outermost first (streaming dim first)                 */
+    int bS[2];                  /* logical tile b_S_i (blocked dims, outer..x)                   */
+    int bS_loaded[2];           /* cells actually loaded per tile (x rounded to 16-byte halos)  */
+    int compute[2];             /* compute region b_S_i - 2*b_T*rad                      */
+    int halo_loaded[2];         /* loaded halo per side (>= b_T*rad)                  */
+    int64_t n_tiles[2];         /* ceil(I_S_i / compute_i)                               */
+    int64_t n_tb;               /* prod n_tiles                                          */
+    int64_t h;                  /* stream-block length h_SN                                      */
+    int64_t n_stream_blocks;    /* ceil(I_S_N / h_SN)                                    */
+    int64_t n_tb_prime;         /* n_stream_blocks * n_tb                                */
+    int64_t stream_overlap;     /* 2*sum_{T=0}^{bT-1} rad*(bT-T) = rad*bT*(bT+1)     */
+    int n_thr;                  /* threads per thread block of the kernel instance               */
+    int units_per_block;        /* independent tiles handled by one thread block                 */
+    int64_t grid_blocks;        /* thread blocks launched per sweep                              */
+    size_t smem_bytes;          /* dynamic shared memory per thread block                        */
+    int regs_per_thread;        /* from cudaFuncGetAttributes of the instance (0 if unknown)     */
+    int vec;                    /* register tiling factor V                                      */
+} an5d_geometry;
+
+/* Create a plan (Table 2).
+ *   ndim 2|3; radius 1..4 ("1st to 4th-order"); shape STAR|BOX.
+ *   coeffs: dense table of (2r+1)^ndim doubles, index order (d_outer, ..., d_x), each d in
+ *     [-r, r]; entry (d) multiplies the neighbour at offset +d: new[x] = sum_d c_d * old[x+d].
+ *     STAR tables must have 0 on every entry with more than one non-zero offset component.
+ *   divisor: 1.0 = none; j-stencils (j2d5pt, j2d9pt, j3d27pt) divide the sum by c_0 (Table 2).
+ *     Applied as in the paper's fast-math build: the reciprocal 1/c_0 is
+ *     folded into the coefficients (in double, then rounded once to dtype).
+ *   Coefficients are rounded once (round-to-nearest) to dtype.  Copies the table; caller keeps
+ *   ownership of `coeffs`.  On success *out owns the plan until an5d_destroy.                  */
+an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* coeffs,
+                        size_t n_coeffs, double divisor, an5d_dtype dtype, an5d_plan** out);
+
+/* Advance the grid by T time steps (host loop of sweeps).
+ *   grid_in / grid_out: device arrays with identical extents/pitches (the paper's A[2]).
+ *   On return grid_out holds step T (interior) and the input ring; grid_in's interior is used as
+ *   scratch and is clobbered when T >= 2 (reading R-7: the sweep count is made odd by
+ *   splitting one sweep, generalising the paper's final-block adjustment).  T == 0 copies.
+ *   cfg: NULL or fields 0 -> host planner.  cuda_stream: cudaStream_t.                          */
+an5d_status an5d_run(an5d_plan* plan, void* grid_in, void* grid_out, const int64_t* extents,
+                     const int64_t* pitches, int64_t T, const an5d_config* cfg, void* cuda_stream);
+
+/* One sweep of degree `degree` (1 <= degree <= cfg->bT) reading src, writing dst, for the slab
+ * mode of multi-GPU runs: the local array holds planes
+ * [outer_offset, outer_offset + extents[0]) of a global array whose outermost extent is
+ * global_outer_extent; only global planes within rad of the global faces are ring planes.
+ * Output planes written: local [out_lo, out_hi) (clipped to the global interior).  Ring cells of
+ * dst must already equal src's (an5d_copy_ring).  Single-GPU: outer_offset = 0,
+ * global_outer_extent = extents[0], out_lo = rad, out_hi = extents[0] - rad.                   */
+an5d_status an5d_sweep(an5d_plan* plan, const void* src, void* dst, const int64_t* extents,
+                       const int64_t* pitches, int degree, const an5d_config* cfg,
+                       int64_t outer_offset, int64_t global_outer_extent, int64_t out_lo,
+                       int64_t out_hi, int32_t* debug_write_count, void* cuda_stream);
+
+/* Copy the rad-wide ring cells of src into dst (O(surface) kernel).  With outer_offset /
+ * global_outer_extent as in an5d_sweep, only global ring planes/rows/columns are copied.       */
+an5d_status an5d_copy_ring(an5d_plan* plan, const void* src, void* dst, const int64_t* extents,
+                           const int64_t* pitches, int64_t outer_offset,
+                           int64_t global_outer_extent, void* cuda_stream);
+
+/* The configuration the host planner picks for (extents, T) on the current device (B200 model,
+ * DESIGN.md "Planner"); fields of `hint` that are non-zero are kept.                            */
+an5d_status an5d_plan_config(an5d_plan* plan, const int64_t* extents, int64_t T,
+                             const an5d_config* hint, an5d_config* out);
+
+/* Bookkeeping introspection for one sweep of degree cfg->bT (bit-exact tests).                 */
+an5d_status an5d_describe(an5d_plan* plan, const int64_t* extents, const an5d_config* cfg,
+                          an5d_geometry* out);
+
+/* Sweep schedule of T steps at degree bT (P:432-441 with reading R-7): writes up to `cap`
+ * degrees to `degrees`, the count to *n_sweeps and whether a trailing interior copy is needed
+ * (bT == 1 with an even T) to *trailing_copy.  Pure host function.                             */
+an5d_status an5d_schedule(int64_t T, int bT, int* degrees, int64_t cap, int64_t* n_sweeps,
+                          int* trailing_copy);
+
+/* Number of kernel launches the last an5d_run on this plan issued (for bench gpu_launches).    */
+int64_t an5d_last_launch_count(const an5d_plan* plan);
+
+an5d_status an5d_destroy(an5d_plan* plan);
+const char* an5d_last_error(void);
+const char* an5d_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AN5D_H */

@@ -1,0 +1,252 @@
+"""paper_2001_01473_b200 -- B200-native N.5D temporally blocked stencils (AN5D, arXiv 2001.01473).
+
+Thin Python binding over the C ABI in ``include/an5d.h`` (libAN5D.so, sm_100a).  Argument
+marshalling only: every step of the sweep runs in the library's CUDA kernels.  PyTorch provides
+device memory and streams.  There is no CPU fallback: if libAN5D.so is missing or fails to load,
+importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libAN5D.so")
+
+STAR, BOX = 0, 1
+F32, F64 = 0, 1
+
+STATUS = {
+    0: "AN5D_OK", 1: "AN5D_ERR_INVALID_ARGUMENT", 2: "AN5D_ERR_INFEASIBLE_CONFIG",
+    3: "AN5D_ERR_BLOCK_TOO_LARGE", 4: "AN5D_ERR_SHAPE_MISMATCH", 5: "AN5D_ERR_UNSUPPORTED",
+    6: "AN5D_ERR_CUDA", 7: "AN5D_ERR_OUT_OF_MEMORY",
+}
+
+
+class AN5DError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("bT", ctypes.c_int), ("bS", ctypes.c_int * 2), ("h", ctypes.c_int64), ("vec", ctypes.c_int)]
+
+    def as_dict(self):
+        return {"bT": self.bT, "bS": list(self.bS), "h": self.h, "vec": self.vec}
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = [
+        ("ndim", ctypes.c_int), ("rad", ctypes.c_int), ("bT", ctypes.c_int),
+        ("interior", ctypes.c_int64 * 3), ("bS", ctypes.c_int * 2), ("bS_loaded", ctypes.c_int * 2),
+        ("compute", ctypes.c_int * 2), ("halo_loaded", ctypes.c_int * 2), ("n_tiles", ctypes.c_int64 * 2),
+        ("n_tb", ctypes.c_int64), ("h", ctypes.c_int64), ("n_stream_blocks", ctypes.c_int64),
+        ("n_tb_prime", ctypes.c_int64), ("stream_overlap", ctypes.c_int64), ("n_thr", ctypes.c_int),
+        ("units_per_block", ctypes.c_int), ("grid_blocks", ctypes.c_int64), ("smem_bytes", ctypes.c_size_t),
+        ("regs_per_thread", ctypes.c_int), ("vec", ctypes.c_int),
+    ]
+
+    def as_dict(self):
+        out = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            out[name] = list(v) if hasattr(v, "__len__") else v
+        return out
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libAN5D.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    pi64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "an5d_create": (I32, [I32, I32, I32, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, D, I32,
+                              ctypes.POINTER(P)]),
+        "an5d_run": (I32, [P, P, P, pi64, pi64, I64, ctypes.POINTER(Config), P]),
+        "an5d_sweep": (I32, [P, P, P, pi64, pi64, I32, ctypes.POINTER(Config), I64, I64, I64, I64, P, P]),
+        "an5d_copy_ring": (I32, [P, P, P, pi64, pi64, I64, I64, P]),
+        "an5d_plan_config": (I32, [P, pi64, I64, ctypes.POINTER(Config), ctypes.POINTER(Config)]),
+        "an5d_describe": (I32, [P, pi64, ctypes.POINTER(Config), ctypes.POINTER(Geometry)]),
+        "an5d_schedule": (I32, [I64, I32, ctypes.POINTER(ctypes.c_int), I64, pi64, ctypes.POINTER(ctypes.c_int)]),
+        "an5d_last_launch_count": (I64, [P]),
+        "an5d_destroy": (I32, [P]),
+        "an5d_last_error": (ctypes.c_char_p, []),
+        "an5d_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_copy_ring", "an5d_plan_config",
+                    "an5d_describe", "an5d_schedule", "an5d_last_launch_count", "an5d_destroy",
+                    "an5d_last_error", "an5d_version")
+
+
+def _check(st: int):
+    if st != 0:
+        raise AN5DError(st, _lib.an5d_last_error().decode())
+
+
+def _i64(vals):
+    arr = (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])
+    return arr
+
+
+def _cfg(cfg) -> Config | None:
+    if cfg is None:
+        return None
+    if isinstance(cfg, Config):
+        return cfg
+    c = Config()
+    c.bT = int(cfg.get("bT", 0))
+    bs = cfg.get("bS", (0, 0)) or (0, 0)
+    c.bS[0] = int(bs[0]) if len(bs) > 0 else 0
+    c.bS[1] = int(bs[1]) if len(bs) > 1 else 0
+    c.h = int(cfg.get("h", 0))
+    c.vec = int(cfg.get("vec", 0))
+    return c
+
+
+def schedule(T: int, bT: int):
+    """Sweep degrees of the host loop (reading R-7) and trailing-copy flag."""
+    n = ctypes.c_int64()
+    tc = ctypes.c_int()
+    _check(_lib.an5d_schedule(int(T), int(bT), None, 0, ctypes.byref(n), ctypes.byref(tc)))
+    buf = (ctypes.c_int * max(1, n.value))()
+    _check(_lib.an5d_schedule(int(T), int(bT), buf, n.value, ctypes.byref(n), ctypes.byref(tc)))
+    return [buf[i] for i in range(n.value)], bool(tc.value)
+
+
+def vec_width(dtype) -> int:
+    return 4 if dtype in (torch.float32, F32) else 2
+
+
+def empty_grid(extents, rad: int, dtype=torch.float32, device="cuda"):
+    """Allocate a grid view meeting the vector-path alignment contract of an5d.h.
+
+    Rows are padded to a multiple of 128 bytes and the view starts so that element x = rad (the
+    first interior cell of every row) is 16-byte aligned.
+    """
+    extents = [int(e) for e in extents]
+    elem = torch.empty((), dtype=dtype).element_size()
+    A = 16 // elem
+    pitch = -(-extents[-1] // (128 // elem)) * (128 // elem)
+    strides = [1]
+    if len(extents) >= 2:
+        strides.insert(0, pitch)
+    if len(extents) == 3:
+        strides.insert(0, pitch * extents[1])
+    n = strides[0] * extents[0] + 2 * A
+    buf = torch.empty(n, dtype=dtype, device=device)
+    off = (A - rad % A) % A
+    return torch.as_strided(buf, extents, strides, storage_offset=off)
+
+
+def to_grid(t: torch.Tensor, rad: int):
+    """Copy a tensor into an aligned grid view (see empty_grid)."""
+    g = empty_grid(t.shape, rad, t.dtype, t.device)
+    g.copy_(t)
+    return g
+
+
+def _geom_of(t: torch.Tensor):
+    if not t.is_cuda:
+        raise ValueError("grids must be CUDA tensors (no CPU path)")
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ValueError("grid dtype must be float32 or float64")
+    if t.dim() not in (2, 3) or t.stride(-1) != 1:
+        raise ValueError("grid must be 2D/3D with unit x stride")
+    return list(t.shape), [t.stride(i) for i in range(t.dim() - 1)]
+
+
+class Stencil:
+    """One stencil (an5d_create): ndim 2|3, radius 1..4, STAR|BOX, dense coefficient table.
+
+    ``coeffs``: array-like of shape (2r+1,)*ndim, index order (d_outer..d_x); entry d multiplies
+    the neighbour at offset +d.  ``divisor``: j-stencil c_0 (Table 2), 1.0 for none.
+    """
+
+    def __init__(self, ndim: int, rad: int, shape: int, coeffs, divisor: float = 1.0, dtype=torch.float32):
+        import numpy as np
+
+        c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64).reshape(-1))
+        self.ndim, self.rad, self.shape, self.divisor = ndim, rad, shape, float(divisor)
+        self.dtype = dtype
+        self.coeffs = c
+        dt = F32 if dtype == torch.float32 else F64
+        h = ctypes.c_void_p()
+        _check(_lib.an5d_create(ndim, rad, shape, c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                c.size, float(divisor), dt, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.an5d_destroy(h)
+            self._h = None
+
+    # -- run / sweep ---------------------------------------------------------------------------
+    def run(self, grid_in: torch.Tensor, grid_out: torch.Tensor, T: int, cfg=None, stream=None):
+        """Advance T steps; result in grid_out (grid_in's interior is clobbered for T >= 2)."""
+        ext, pit = _geom_of(grid_in)
+        if list(grid_out.shape) != ext or [grid_out.stride(i) for i in range(grid_out.dim() - 1)] != pit:
+            raise ValueError("grid_in and grid_out must have identical shape and strides")
+        if grid_in.dtype != self.dtype or grid_out.dtype != self.dtype:
+            raise ValueError("grid dtype does not match the stencil dtype")
+        st = stream if stream is not None else torch.cuda.current_stream(grid_in.device)
+        c = _cfg(cfg)
+        _check(_lib.an5d_run(self._h, grid_in.data_ptr(), grid_out.data_ptr(), _i64(ext), _i64(pit), int(T),
+                             ctypes.byref(c) if c is not None else None, ctypes.c_void_p(st.cuda_stream)))
+        return grid_out
+
+    def sweep(self, src: torch.Tensor, dst: torch.Tensor, degree: int, cfg, outer_offset: int = 0,
+              global_outer_extent: int | None = None, out_lo: int | None = None, out_hi: int | None = None,
+              write_count: torch.Tensor | None = None, stream=None):
+        """One sweep of `degree` time steps (slab mode; see an5d.h an5d_sweep)."""
+        ext, pit = _geom_of(src)
+        g = ext[0] if global_outer_extent is None else global_outer_extent
+        lo = self.rad if out_lo is None else out_lo
+        hi = ext[0] - self.rad if out_hi is None else out_hi
+        st = stream if stream is not None else torch.cuda.current_stream(src.device)
+        c = _cfg(cfg)
+        wc = write_count.data_ptr() if write_count is not None else None
+        _check(_lib.an5d_sweep(self._h, src.data_ptr(), dst.data_ptr(), _i64(ext), _i64(pit), int(degree),
+                               ctypes.byref(c), int(outer_offset), int(g), int(lo), int(hi), wc,
+                               ctypes.c_void_p(st.cuda_stream)))
+
+    def copy_ring(self, src: torch.Tensor, dst: torch.Tensor, outer_offset: int = 0,
+                  global_outer_extent: int | None = None, stream=None):
+        ext, pit = _geom_of(src)
+        g = ext[0] if global_outer_extent is None else global_outer_extent
+        st = stream if stream is not None else torch.cuda.current_stream(src.device)
+        _check(_lib.an5d_copy_ring(self._h, src.data_ptr(), dst.data_ptr(), _i64(ext), _i64(pit),
+                                   int(outer_offset), int(g), ctypes.c_void_p(st.cuda_stream)))
+
+    # -- planner / bookkeeping -------------------------------------------------------------------
+    def plan_config(self, extents, T: int = 0, hint=None) -> dict:
+        out = Config()
+        h = _cfg(hint)
+        _check(_lib.an5d_plan_config(self._h, _i64(extents), int(T), ctypes.byref(h) if h else None,
+                                     ctypes.byref(out)))
+        return out.as_dict()
+
+    def describe(self, extents, cfg) -> dict:
+        out = Geometry()
+        c = _cfg(cfg)
+        _check(_lib.an5d_describe(self._h, _i64(extents), ctypes.byref(c), ctypes.byref(out)))
+        return out.as_dict()
+
+    def last_launch_count(self) -> int:
+        return int(_lib.an5d_last_launch_count(self._h))
+
+
+def version() -> str:
+    return _lib.an5d_version().decode()

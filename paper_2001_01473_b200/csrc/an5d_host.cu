@@ -1,0 +1,798 @@
+// an5d_host.cu -- libAN5D host side: C ABI (include/an5d.h), sweep geometry, sweep schedule,
+// B200 planner, launch orchestration.  Product code: shares nothing with oracle/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/an5d.h"
+#include "registry.hpp"
+
+namespace an5d {
+
+std::vector<Instance>& registry() {
+    static std::vector<Instance> r;
+    return r;
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+an5d_status fail(an5d_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+an5d_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(AN5D_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t m) { return cdiv(a, m) * m; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------------------------
+struct Plan {
+    int ndim, rad, shape, dtype;
+    size_t elem;                       // bytes per cell (n_word)
+    std::vector<double> coeffs_folded; // dense table / divisor (P:596-602 reciprocal folding)
+    std::vector<unsigned char> coeffs_dev_t;  // rounded to dtype, as raw bytes
+    double divisor;
+    cudaStream_t side = nullptr;       // edge-tile launches run here, concurrently
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int device = -1;
+    int64_t launches = 0;
+};
+
+}  // namespace an5d
+
+struct an5d_plan : an5d::Plan {};
+
+namespace an5d {
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// Sweep schedule (P:432-441 with DESIGN.md reading R-7)
+//   degrees = [bT] * floor(T/bT) (+ [T mod bT]).  The result must land in grid_out after an odd
+//   number of sweeps (each sweep flips the buffers, as the paper's (t+1)%2 indexing does).  If the
+//   count is even, split the LAST sweep of degree >= 2 into (ceil(d/2), floor(d/2)) in place; if
+//   every degree is 1 (bT == 1), append an interior copy instead.
+// ---------------------------------------------------------------------------------------------
+void make_schedule(int64_t T, int bT, std::vector<int>& deg, bool& trailing_copy) {
+    deg.clear();
+    trailing_copy = false;
+    if (T <= 0) return;
+    for (int64_t i = 0; i < T / bT; ++i) deg.push_back(bT);
+    if (T % bT) deg.push_back((int)(T % bT));
+    if (deg.size() % 2 == 0) {
+        for (int64_t i = (int64_t)deg.size() - 1; i >= 0; --i) {
+            if (deg[i] >= 2) {
+                const int d = deg[i];
+                deg[i] = (d + 1) / 2;
+                deg.insert(deg.begin() + i + 1, d / 2);
+                return;
+            }
+        }
+        trailing_copy = true;
+    }
+}
+
+const Instance* find_instance(const Plan& p, int bT, int vec) {
+    for (const Instance& i : registry())
+        if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad &&
+            i.bT == bT && i.vec == vec)
+            return &i;
+    return nullptr;
+}
+
+int max_bT_for(const Plan& p, int vec) {
+    int m = 0;
+    for (const Instance& i : registry())
+        if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad &&
+            i.vec == vec)
+            m = std::max(m, i.bT);
+    return m;
+}
+
+// Sizes of the local problem
+struct Dims {
+    int64_t E[3];      // extents outer..x (ndim entries used)
+    int64_t pitch[2];  // outer strides (2D: pitch[0] = row; 3D: pitch[0] = plane, pitch[1] = row)
+};
+
+// ---------------------------------------------------------------------------------------------
+// Geometry of one sweep of degree d (bit-exact bookkeeping)
+// ---------------------------------------------------------------------------------------------
+struct SweepGeom {
+    int A;                 // cells per 16-byte vector
+    int loaded[2];         // loaded tile per blocked dim (outer..x)
+    int halo[2];           // loaded halo per side
+    int C[2];              // compute region per blocked dim
+    int64_t ntiles[2];
+    int64_t h, n_sb;
+    // interior rectangle / box
+    int64_t sb_lo, sb_hi;
+    int64_t t_lo[2], t_hi[2];
+    int64_t n_units, n_interior;
+};
+
+an5d_status sweep_geometry(const Plan& p, const Instance& inst, const Dims& dm, int d, int64_t h,
+                           int64_t g_off, int64_t gE0, int64_t out_lo, int64_t out_hi, SweepGeom& g) {
+    const int R = p.rad;
+    g.A = (int)(16 / p.elem);
+    const int nb = p.ndim - 1;  // blocked dims
+    int loaded[2], halo[2];
+    if (p.ndim == 2) {
+        loaded[0] = inst.tile_x_loaded;
+        halo[0] = (int)round_up((int64_t)d * R, g.A);
+    } else {
+        loaded[0] = inst.tile_y;
+        halo[0] = d * R;
+        loaded[1] = inst.tile_x_loaded;
+        halo[1] = (int)round_up((int64_t)d * R, g.A);
+    }
+    for (int i = 0; i < nb; ++i) {
+        g.loaded[i] = loaded[i];
+        g.halo[i] = halo[i];
+        g.C[i] = loaded[i] - 2 * halo[i];
+        if (g.C[i] < 1)
+            return fail(AN5D_ERR_INFEASIBLE_CONFIG,
+                        "empty compute region: tile %d - 2*halo %d < 1 (P:320 b_S - 2 b_T rad >= 1)",
+                        loaded[i], halo[i]);
+        const int64_t I = dm.E[1 + i] - 2 * R;
+        g.ntiles[i] = cdiv(I, g.C[i]);
+        // interior tiles: loaded window [R + t C - H, +loaded) inside [R, E - R)
+        const int64_t E = dm.E[1 + i];
+        int64_t lo = 0, hi = g.ntiles[i];
+        while (lo < hi && (R + lo * g.C[i] - halo[i] < R || R + lo * g.C[i] - halo[i] + loaded[i] > E - R)) ++lo;
+        while (hi > lo && (R + (hi - 1) * g.C[i] - halo[i] + loaded[i] > E - R)) --hi;
+        g.t_lo[i] = lo;
+        g.t_hi[i] = hi;
+    }
+    const int64_t Iout = out_hi - out_lo;
+    g.h = std::max<int64_t>(1, std::min<int64_t>(h, Iout));
+    g.n_sb = cdiv(Iout, g.h);
+    auto sb_edge = [&](int64_t sb) {
+        const int64_t p0 = out_lo + sb * g.h, p1 = std::min(p0 + g.h, out_hi);
+        const int64_t s0 = p0 - (int64_t)d * R, s1 = p1 + (int64_t)d * R;
+        return s0 < 0 || s1 > dm.E[0] || s0 + g_off < R || s1 - 1 + g_off >= gE0 - R;
+    };
+    int64_t lo = 0, hi = g.n_sb;
+    while (lo < hi && sb_edge(lo)) ++lo;
+    while (hi > lo && sb_edge(hi - 1)) --hi;
+    g.sb_lo = lo;
+    g.sb_hi = hi;
+    int64_t nt = 1, ni = hi - lo;
+    for (int i = 0; i < nb; ++i) {
+        nt *= g.ntiles[i];
+        ni *= std::max<int64_t>(0, g.t_hi[i] - g.t_lo[i]);
+    }
+    // an empty interior box: everything is edge
+    bool empty = (hi <= lo);
+    for (int i = 0; i < nb; ++i) empty = empty || g.t_hi[i] <= g.t_lo[i];
+    if (empty) {
+        g.sb_lo = g.sb_hi = 0;
+        for (int i = 0; i < nb; ++i) g.t_lo[i] = g.t_hi[i] = 0;
+        ni = 0;
+    }
+    g.n_units = nt * g.n_sb;
+    g.n_interior = ni;
+    return AN5D_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Device properties used by the planner
+// ---------------------------------------------------------------------------------------------
+struct DevInfo {
+    int n_sm = 148;
+    double clock_ghz = 1.965;
+    double hbm_gbs = 6549.0;   // MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)
+};
+
+DevInfo dev_info() {
+    DevInfo di;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) di.n_sm = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev) == cudaSuccess && v > 0) di.clock_ghz = v * 1e-6;
+    }
+    if (const char* e = getenv("AN5D_HBM_GBS")) di.hbm_gbs = atof(e);
+    return di;
+}
+
+int resident_blocks(const Instance& inst) {
+    int nblk = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, inst.fn_interior, inst.threads,
+                                                      inst.smem_bytes) != cudaSuccess || nblk < 1) {
+        cudaGetLastError();
+        if (inst.smem_bytes > 48 * 1024) {
+            cudaFuncSetAttribute(inst.fn_interior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inst.smem_bytes);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, inst.fn_interior, inst.threads,
+                                                              inst.smem_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                nblk = 1;
+            }
+        } else {
+            nblk = 1;
+        }
+    }
+    return std::max(1, nblk);
+}
+
+int taps_of(const Plan& p) {
+    const int w = 2 * p.rad + 1;
+    if (p.shape == AN5D_BOX) return p.ndim == 2 ? w * w : w * w * w;
+    return p.ndim == 2 ? 4 * p.rad + 1 : 6 * p.rad + 1;
+}
+
+// Planner model: predicted seconds per cell-step of a configuration.
+//   HBM term: bytes moved per sweep (tile windows incl. halo and stream overlap read, compute
+//   region written) / measured HBM bandwidth;
+//   issue term: warp-instructions per sweep (taps FFMA/DFMA + shuffle/shared-memory exchange + a
+//   fixed per-level overhead) / (4 schedulers x n_SM x clock), with FP64 at half rate;
+//   waves: units / (resident units per SM x n_SM), rounded up (the paper's eff_SM).
+double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, int64_t h, const DevInfo& di,
+                  SweepGeom* out_geom) {
+    SweepGeom g{};
+    if (sweep_geometry(p, inst, dm, bT, h, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g) != AN5D_OK) return 1e30;
+    const int R = p.rad;
+    int64_t interior = 1;
+    for (int i = 0; i < p.ndim; ++i) interior *= dm.E[i] - 2 * R;
+    const int64_t steps_per_unit = g.h + 2LL * bT * R;
+    int64_t cells_per_plane = 1;
+    for (int i = 0; i < p.ndim - 1; ++i) cells_per_plane *= g.loaded[i];
+    const double bytes = (double)p.elem * ((double)g.n_units * steps_per_unit * cells_per_plane + (double)interior);
+    const double t_hbm = bytes / (di.hbm_gbs * 1e9);
+    // issue model per plane per level, in warp-instructions per thread-cell
+    const int taps = taps_of(p);
+    double fp = taps;
+    double xch;
+    const int cells_per_thread = p.ndim == 2 ? inst.vec : inst.vec * 4;
+    if (p.ndim == 2) {
+        xch = (2.0 * R + 2.0) / cells_per_thread;  // shuffles + misc per lane-level
+    } else {
+        const int vy = inst.vec;
+        const double halo_words = (p.shape == AN5D_BOX) ? ((vy + 2.0 * R) * (4 + 2.0 * R) - vy * 4)
+                                                        : (2.0 * R * vy + 2.0 * R * 4);
+        xch = (halo_words + vy + 6.0) / cells_per_thread;
+    }
+    const double fp_rate = p.dtype == AN5D_F64 ? 2.0 : 1.0;  // DFMA occupies the pipe 2 cycles
+    const double instr_per_cell_level = std::max(fp * fp_rate, fp + xch) + 0.0;
+    const double thread_cells = (double)g.n_units * steps_per_unit * cells_per_plane * bT;
+    const double warp_instr = thread_cells * instr_per_cell_level / 32.0;
+    const double t_issue = warp_instr / (4.0 * di.n_sm * di.clock_ghz * 1e9);
+    // waves
+    const int per_sm = resident_blocks(inst) * (p.ndim == 2 ? kWarps2D : 1);
+    const double conc = (double)per_sm * di.n_sm;
+    const double waves = (double)g.n_units / conc;
+    const double eff = waves / std::ceil(waves);
+    const double t = std::max(t_hbm, t_issue) / std::max(0.05, eff);
+    if (out_geom) *out_geom = g;
+    return t / ((double)interior * bT);
+}
+
+an5d_status choose_config(const Plan& p, const Dims& dm, int64_t T, const an5d_config* hint, an5d_config& out) {
+    const DevInfo di = dev_info();
+    double best = 1e300;
+    an5d_config bc{};
+    const int64_t Iout = dm.E[0] - 2 * p.rad;
+    for (const Instance& inst : registry()) {
+        if (inst.ndim != p.ndim || inst.shape != p.shape || inst.dtype != p.dtype || inst.rad != p.rad) continue;
+        if (hint && hint->bT && inst.bT != hint->bT) continue;
+        if (hint && hint->vec && inst.vec != hint->vec) continue;
+        if (T > 0 && inst.bT > T) continue;
+        // every reduced degree the schedule may need must exist with the same vec
+        bool ok = true;
+        for (int d = 1; d < inst.bT && ok; ++d) ok = find_instance(p, d, inst.vec) != nullptr;
+        if (!ok) continue;
+        std::vector<int64_t> hs;
+        if (hint && hint->h) {
+            hs.push_back(hint->h);
+        } else {
+            // candidate stream-block lengths: 1..4 waves of resident units
+            SweepGeom g{};
+            if (sweep_geometry(p, inst, dm, inst.bT, Iout, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g) != AN5D_OK) continue;
+            int64_t nt = 1;
+            for (int i = 0; i < p.ndim - 1; ++i) nt *= g.ntiles[i];
+            const int per_sm = resident_blocks(inst) * (p.ndim == 2 ? kWarps2D : 1);
+            const int64_t conc = (int64_t)per_sm * di.n_sm;
+            for (int w = 1; w <= 8; ++w) {
+                const int64_t nsb = std::max<int64_t>(1, (w * conc) / std::max<int64_t>(1, nt));
+                hs.push_back(std::max<int64_t>(1, cdiv(Iout, nsb)));
+            }
+            hs.push_back(Iout);
+        }
+        for (int64_t h : hs) {
+            const double t = model_time(p, inst, dm, inst.bT, h, di, nullptr);
+            if (t < best) {
+                best = t;
+                bc.bT = inst.bT;
+                bc.vec = inst.vec;
+                bc.h = h;
+            }
+        }
+    }
+    if (best >= 1e29)
+        return fail(AN5D_ERR_UNSUPPORTED, "no feasible kernel instance for ndim=%d rad=%d shape=%d dtype=%d",
+                    p.ndim, p.rad, p.shape, p.dtype);
+    out = bc;
+    return AN5D_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Copy kernels (ring copy: O(surface); whole-array copy for T == 0 / trailing copy)
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void ring_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t nrows, int64_t Ey,
+                                 int64_t Ex, int64_t pz, int64_t py, int R, int64_t g_off, int64_t gE0,
+                                 int is3d) {
+    for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+        int64_t z = 0, y = row;
+        if (is3d) { z = row / Ey; y = row % Ey; }
+        const int64_t gouter = (is3d ? z : y) + g_off;
+        bool full = gouter < R || gouter >= gE0 - R;
+        if (is3d) full = full || y < R || y >= Ey - R;
+        const int64_t off = is3d ? z * pz + y * py : y * py;
+        if (full) {
+            for (int64_t x = threadIdx.x; x < Ex; x += blockDim.x) dst[off + x] = src[off + x];
+        } else {
+            for (int64_t x = threadIdx.x; x < 2 * R; x += blockDim.x) {
+                const int64_t xx = x < R ? x : Ex - 2 * R + x;
+                dst[off + xx] = src[off + xx];
+            }
+        }
+    }
+}
+
+template <typename T>
+__global__ void copy_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t nrows, int64_t Ey,
+                            int64_t Ex, int64_t pz, int64_t py, int is3d) {
+    for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+        int64_t off = row * py;
+        if (is3d) off = (row / Ey) * pz + (row % Ey) * py;
+        for (int64_t x = threadIdx.x; x < Ex; x += blockDim.x) dst[off + x] = src[off + x];
+    }
+}
+
+an5d_status launch_copy(Plan& p, const void* src, void* dst, const Dims& dm, bool ring_only, int64_t g_off,
+                        int64_t gE0, cudaStream_t st) {
+    const bool is3d = p.ndim == 3;
+    const int64_t Ey = is3d ? dm.E[1] : dm.E[0];
+    const int64_t Ex = dm.E[p.ndim - 1];
+    const int64_t nrows = is3d ? dm.E[0] * dm.E[1] : dm.E[0];
+    const int64_t pz = is3d ? dm.pitch[0] : 0;
+    const int64_t py = is3d ? dm.pitch[1] : dm.pitch[0];
+    const unsigned grid = (unsigned)std::min<int64_t>(nrows, 148 * 32);
+    const int thr = ring_only ? 128 : 256;
+    if (p.dtype == AN5D_F32) {
+        if (ring_only)
+            ring_copy_kernel<float><<<grid, thr, 0, st>>>((const float*)src, (float*)dst, nrows, Ey, Ex, pz, py,
+                                                          p.rad, g_off, gE0, is3d);
+        else
+            copy_kernel<float><<<grid, thr, 0, st>>>((const float*)src, (float*)dst, nrows, Ey, Ex, pz, py, is3d);
+    } else {
+        if (ring_only)
+            ring_copy_kernel<double><<<grid, thr, 0, st>>>((const double*)src, (double*)dst, nrows, Ey, Ex, pz,
+                                                           py, p.rad, g_off, gE0, is3d);
+        else
+            copy_kernel<double><<<grid, thr, 0, st>>>((const double*)src, (double*)dst, nrows, Ey, Ex, pz, py,
+                                                      is3d);
+    }
+    p.launches++;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? AN5D_OK : cuda_fail(e, "copy kernel launch");
+}
+
+an5d_status ensure_streams(Plan& p) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (p.side && p.device == dev) return AN5D_OK;
+    if (p.side) {
+        cudaStreamDestroy(p.side);
+        cudaEventDestroy(p.ev_fork);
+        cudaEventDestroy(p.ev_join);
+    }
+    if ((e = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+    if ((e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    p.device = dev;
+    return AN5D_OK;
+}
+
+// One sweep: edge units on the side stream, interior units on the caller's stream, joined.
+an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, int d, const an5d_config& cfg,
+                         int64_t g_off, int64_t gE0, int64_t out_lo, int64_t out_hi, int32_t* wc,
+                         cudaStream_t st) {
+    const Instance* inst = find_instance(p, d, cfg.vec);
+    if (!inst) return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for degree %d vec %d", d, cfg.vec);
+    SweepGeom g{};
+    an5d_status s = sweep_geometry(p, *inst, dm, d, cfg.h, g_off, gE0, out_lo, out_hi, g);
+    if (s != AN5D_OK) return s;
+    const int64_t n_edge = g.n_units - g.n_interior;
+    cudaError_t e;
+    if (p.ndim == 2) {
+        Sweep2DArgs a{};
+        a.src = src; a.dst = dst; a.pitch = dm.pitch[0];
+        a.Ey = dm.E[0]; a.g_off = g_off; a.gEy = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
+        a.h = g.h; a.n_sb = g.n_sb; a.sb_lo = g.sb_lo; a.sb_hi = g.sb_hi;
+        a.tx_lo = (int)g.t_lo[0]; a.tx_hi = (int)g.t_hi[0];
+        a.wc = wc; a.Ex = (int)dm.E[1]; a.C = g.C[0]; a.H = g.halo[0]; a.n_tiles_x = (int)g.ntiles[0];
+        if (n_edge > 0) {
+            if ((e = cudaEventRecord(p.ev_fork, st)) != cudaSuccess) return cuda_fail(e, "event record");
+            if ((e = cudaStreamWaitEvent(p.side, p.ev_fork, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+            Sweep2DArgs ae = a;
+            ae.n_units = n_edge;
+            if ((e = inst->launch2d(ae, p.coeffs_dev_t.data(), cdiv(n_edge, kWarps2D), true, p.side)) != cudaSuccess)
+                return cuda_fail(e, "edge sweep launch");
+            p.launches++;
+            if ((e = cudaEventRecord(p.ev_join, p.side)) != cudaSuccess) return cuda_fail(e, "event record");
+        }
+        if (g.n_interior > 0) {
+            a.n_units = g.n_interior;
+            if ((e = inst->launch2d(a, p.coeffs_dev_t.data(), cdiv(g.n_interior, kWarps2D), false, st)) != cudaSuccess)
+                return cuda_fail(e, "interior sweep launch");
+            p.launches++;
+        }
+    } else {
+        Sweep3DArgs a{};
+        a.src = src; a.dst = dst; a.pz = dm.pitch[0]; a.py = dm.pitch[1];
+        a.Ez = dm.E[0]; a.g_off = g_off; a.gEz = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
+        a.h = g.h; a.n_sb = g.n_sb; a.sb_lo = g.sb_lo; a.sb_hi = g.sb_hi; a.wc = wc;
+        a.Ey = (int)dm.E[1]; a.Ex = (int)dm.E[2];
+        a.Cy = g.C[0]; a.Cx = g.C[1]; a.Hy = g.halo[0]; a.Hx = g.halo[1];
+        a.nty = (int)g.ntiles[0]; a.ntx = (int)g.ntiles[1];
+        a.ty_lo = (int)g.t_lo[0]; a.ty_hi = (int)g.t_hi[0]; a.tx_lo = (int)g.t_lo[1]; a.tx_hi = (int)g.t_hi[1];
+        if (n_edge > 0) {
+            if ((e = cudaEventRecord(p.ev_fork, st)) != cudaSuccess) return cuda_fail(e, "event record");
+            if ((e = cudaStreamWaitEvent(p.side, p.ev_fork, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+            Sweep3DArgs ae = a;
+            ae.n_units = n_edge;
+            if ((e = inst->launch3d(ae, p.coeffs_dev_t.data(), n_edge, true, p.side)) != cudaSuccess)
+                return cuda_fail(e, "edge sweep launch");
+            p.launches++;
+            if ((e = cudaEventRecord(p.ev_join, p.side)) != cudaSuccess) return cuda_fail(e, "event record");
+        }
+        if (g.n_interior > 0) {
+            a.n_units = g.n_interior;
+            if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), g.n_interior, false, st)) != cudaSuccess)
+                return cuda_fail(e, "interior sweep launch");
+            p.launches++;
+        }
+    }
+    if (n_edge > 0) {
+        if ((e = cudaStreamWaitEvent(st, p.ev_join, 0)) != cudaSuccess) return cuda_fail(e, "join");
+    }
+    return AN5D_OK;
+}
+
+an5d_status read_dims(const Plan& p, const int64_t* extents, const int64_t* pitches, Dims& dm) {
+    if (!extents) return fail(AN5D_ERR_INVALID_ARGUMENT, "extents is NULL");
+    for (int i = 0; i < p.ndim; ++i) {
+        dm.E[i] = extents[i];
+        if (dm.E[i] < 2 * p.rad + 1)
+            return fail(AN5D_ERR_SHAPE_MISMATCH, "extent[%d]=%lld < 2*rad+1 (no interior cell)", i,
+                        (long long)dm.E[i]);
+        if (dm.E[i] > (1LL << 30) && i > 0)
+            return fail(AN5D_ERR_UNSUPPORTED, "blocked extent[%d] too large", i);
+    }
+    if (p.ndim == 2) {
+        dm.pitch[0] = pitches ? pitches[0] : dm.E[1];
+        if (dm.pitch[0] < dm.E[1]) return fail(AN5D_ERR_SHAPE_MISMATCH, "row pitch < x extent");
+    } else {
+        dm.pitch[1] = pitches ? pitches[1] : dm.E[2];
+        dm.pitch[0] = pitches ? pitches[0] : dm.E[1] * dm.pitch[1];
+        if (dm.pitch[1] < dm.E[2]) return fail(AN5D_ERR_SHAPE_MISMATCH, "row pitch < x extent");
+        if (dm.pitch[0] < dm.E[1] * dm.pitch[1]) return fail(AN5D_ERR_SHAPE_MISMATCH, "plane pitch < rows*pitch");
+    }
+    return AN5D_OK;
+}
+
+an5d_status check_alignment(const Plan& p, const void* ptr, const Dims& dm, const char* name) {
+    if (!ptr) return fail(AN5D_ERR_INVALID_ARGUMENT, "%s is NULL", name);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(ptr) + (uintptr_t)p.rad * p.elem;
+    if (a % 16) return fail(AN5D_ERR_UNSUPPORTED, "%s: element x=rad of row 0 is not 16-byte aligned", name);
+    for (int i = 0; i < p.ndim - 1; ++i)
+        if ((dm.pitch[i] * (int64_t)p.elem) % 16)
+            return fail(AN5D_ERR_UNSUPPORTED, "%s: pitch[%d]*elem_size not a multiple of 16 bytes", name, i);
+    return AN5D_OK;
+}
+
+an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config* cfg, an5d_config& c) {
+    an5d_config hint{};
+    if (cfg) hint = *cfg;
+    if (const char* f = getenv("AN5D_FORCE_CFG")) {  // "bT,vec,h" benchmarking override
+        int bt = 0, v = 0;
+        long long h = 0;
+        if (sscanf(f, "%d,%d,%lld", &bt, &v, &h) >= 1) {
+            if (bt) hint.bT = bt;
+            if (v) hint.vec = v;
+            if (h) hint.h = h;
+        }
+    }
+    if (hint.bT < 0 || hint.vec < 0 || hint.h < 0) return fail(AN5D_ERR_INVALID_ARGUMENT, "negative config field");
+    if (hint.bT && hint.vec && hint.h) {
+        c = hint;
+    } else {
+        an5d_status s = choose_config(p, dm, T, &hint, c);
+        if (s != AN5D_OK) return s;
+    }
+    if (!find_instance(p, c.bT, c.vec))
+        return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for ndim=%d rad=%d shape=%d dtype=%d bT=%d vec=%d",
+                    p.ndim, p.rad, p.shape, p.dtype, c.bT, c.vec);
+    for (int d = 1; d < c.bT; ++d)
+        if (!find_instance(p, d, c.vec))
+            return fail(AN5D_ERR_UNSUPPORTED, "no reduced-degree instance d=%d for vec %d", d, c.vec);
+    // logical tile b_S reported back
+    const Instance* inst = find_instance(p, c.bT, c.vec);
+    SweepGeom g{};
+    an5d_status s = sweep_geometry(p, *inst, dm, c.bT, c.h ? c.h : dm.E[0], 0, dm.E[0], p.rad, dm.E[0] - p.rad, g);
+    if (s != AN5D_OK) return s;
+    const int nb = p.ndim - 1;
+    for (int i = 0; i < 2; ++i) {
+        const int want = i < nb ? g.C[i] + 2 * c.bT * p.rad : 0;
+        if (cfg && cfg->bS[i] && cfg->bS[i] != want)
+            return fail(AN5D_ERR_UNSUPPORTED, "bS[%d]=%d not available: instance vec=%d gives b_S=%d", i, cfg->bS[i],
+                        c.vec, want);
+        c.bS[i] = want;
+    }
+    if (!c.h) c.h = dm.E[0] - 2 * p.rad;
+    return AN5D_OK;
+}
+
+}  // namespace
+}  // namespace an5d
+
+using namespace an5d;
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char* an5d_last_error(void) { return g_err.c_str(); }
+const char* an5d_version(void) { return "an5d-b200 0.1 (sm_100a)"; }
+
+an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* coeffs, size_t n_coeffs,
+                        double divisor, an5d_dtype dtype, an5d_plan** out) {
+    try {
+        if (!out) return fail(AN5D_ERR_INVALID_ARGUMENT, "out is NULL");
+        *out = nullptr;
+        if (ndim != 2 && ndim != 3) return fail(AN5D_ERR_INVALID_ARGUMENT, "ndim must be 2 or 3");
+        if (radius < 1 || radius > 4) return fail(AN5D_ERR_INVALID_ARGUMENT, "radius must be 1..4");
+        if (shape != AN5D_STAR && shape != AN5D_BOX) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad shape");
+        if (dtype != AN5D_F32 && dtype != AN5D_F64) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad dtype");
+        if (!coeffs) return fail(AN5D_ERR_INVALID_ARGUMENT, "coeffs is NULL");
+        if (!(divisor != 0.0) || !std::isfinite(divisor)) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad divisor");
+        const int w = 2 * radius + 1;
+        const size_t n = ndim == 2 ? (size_t)w * w : (size_t)w * w * w;
+        if (n_coeffs != n)
+            return fail(AN5D_ERR_SHAPE_MISMATCH, "expected %zu coefficients ((2r+1)^ndim), got %zu", n, n_coeffs);
+        for (size_t k = 0; k < n; ++k) {
+            int rem = (int)k, nz = 0;
+            for (int i = 0; i < ndim; ++i) { nz += (rem % w) != radius; rem /= w; }
+            if (!std::isfinite(coeffs[k])) return fail(AN5D_ERR_INVALID_ARGUMENT, "non-finite coefficient");
+            if (shape == AN5D_STAR && nz > 1 && coeffs[k] != 0.0)
+                return fail(AN5D_ERR_SHAPE_MISMATCH, "STAR table has non-zero off-axis entry %zu", k);
+        }
+        an5d_plan* p = new an5d_plan();
+        p->ndim = ndim; p->rad = radius; p->shape = shape; p->dtype = dtype;
+        p->elem = dtype == AN5D_F32 ? 4 : 8;
+        p->divisor = divisor;
+        p->coeffs_folded.resize(n);
+        const double inv = 1.0 / divisor;
+        for (size_t k = 0; k < n; ++k) p->coeffs_folded[k] = divisor == 1.0 ? coeffs[k] : coeffs[k] * inv;
+        p->coeffs_dev_t.resize(n * p->elem);
+        for (size_t k = 0; k < n; ++k) {
+            if (dtype == AN5D_F32) {
+                const float f = (float)p->coeffs_folded[k];
+                memcpy(p->coeffs_dev_t.data() + k * 4, &f, 4);
+            } else {
+                memcpy(p->coeffs_dev_t.data() + k * 8, &p->coeffs_folded[k], 8);
+            }
+        }
+        *out = p;
+        return AN5D_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(AN5D_ERR_OUT_OF_MEMORY, "host allocation failed");
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_destroy(an5d_plan* p) {
+    if (!p) return AN5D_OK;
+    if (p->side) {
+        cudaStreamDestroy(p->side);
+        cudaEventDestroy(p->ev_fork);
+        cudaEventDestroy(p->ev_join);
+    }
+    delete p;
+    return AN5D_OK;
+}
+
+int64_t an5d_last_launch_count(const an5d_plan* p) { return p ? p->launches : 0; }
+
+an5d_status an5d_schedule(int64_t T, int bT, int* degrees, int64_t cap, int64_t* n_sweeps, int* trailing_copy) {
+    try {
+        if (T < 0 || bT < 1) return fail(AN5D_ERR_INVALID_ARGUMENT, "T < 0 or bT < 1");
+        std::vector<int> deg;
+        bool tc = false;
+        make_schedule(T, bT, deg, tc);
+        if (n_sweeps) *n_sweeps = (int64_t)deg.size();
+        if (trailing_copy) *trailing_copy = tc ? 1 : 0;
+        if (degrees)
+            for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)deg.size()); ++i) degrees[i] = deg[i];
+        return AN5D_OK;
+    } catch (...) {
+        return fail(AN5D_ERR_OUT_OF_MEMORY, "schedule");
+    }
+}
+
+an5d_status an5d_plan_config(an5d_plan* p, const int64_t* extents, int64_t T, const an5d_config* hint,
+                             an5d_config* out) {
+    try {
+        if (!p || !out) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, nullptr, dm);
+        if (s != AN5D_OK) return s;
+        return resolve_config(*p, dm, T, hint, *out);
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_config* cfg, an5d_geometry* out) {
+    try {
+        if (!p || !out || !cfg) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, nullptr, dm);
+        if (s != AN5D_OK) return s;
+        an5d_config c{};
+        if ((s = resolve_config(*p, dm, 0, cfg, c)) != AN5D_OK) return s;
+        const Instance* inst = find_instance(*p, c.bT, c.vec);
+        SweepGeom g{};
+        if ((s = sweep_geometry(*p, *inst, dm, c.bT, c.h, 0, dm.E[0], p->rad, dm.E[0] - p->rad, g)) != AN5D_OK)
+            return s;
+        memset(out, 0, sizeof *out);
+        out->ndim = p->ndim; out->rad = p->rad; out->bT = c.bT; out->vec = c.vec;
+        for (int i = 0; i < p->ndim; ++i) out->interior[i] = dm.E[i] - 2 * p->rad;
+        int64_t ntb = 1;
+        for (int i = 0; i < p->ndim - 1; ++i) {
+            out->bS[i] = g.C[i] + 2 * c.bT * p->rad;
+            out->bS_loaded[i] = g.loaded[i];
+            out->compute[i] = g.C[i];
+            out->halo_loaded[i] = g.halo[i];
+            out->n_tiles[i] = g.ntiles[i];
+            ntb *= g.ntiles[i];
+        }
+        out->n_tb = ntb;
+        out->h = g.h;
+        out->n_stream_blocks = g.n_sb;
+        out->n_tb_prime = g.n_sb * ntb;
+        int64_t ov = 0;
+        for (int T = 0; T < c.bT; ++T) ov += (int64_t)p->rad * (c.bT - T);
+        out->stream_overlap = 2 * ov;
+        out->n_thr = inst->threads;
+        out->units_per_block = p->ndim == 2 ? kWarps2D : 1;
+        out->grid_blocks = p->ndim == 2 ? cdiv(g.n_interior, kWarps2D) + cdiv(g.n_units - g.n_interior, kWarps2D)
+                                        : g.n_units;
+        out->smem_bytes = inst->smem_bytes;
+        cudaFuncAttributes attr{};
+        if (cudaFuncGetAttributes(&attr, inst->fn_interior) == cudaSuccess) out->regs_per_thread = attr.numRegs;
+        else cudaGetLastError();
+        return AN5D_OK;
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_copy_ring(an5d_plan* p, const void* src, void* dst, const int64_t* extents, const int64_t* pitches,
+                           int64_t outer_offset, int64_t global_outer_extent, void* stream) {
+    try {
+        if (!p || !src || !dst) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, pitches, dm);
+        if (s != AN5D_OK) return s;
+        return launch_copy(*p, src, dst, dm, true, outer_offset, global_outer_extent, (cudaStream_t)stream);
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_sweep(an5d_plan* p, const void* src, void* dst, const int64_t* extents, const int64_t* pitches,
+                       int degree, const an5d_config* cfg, int64_t outer_offset, int64_t global_outer_extent,
+                       int64_t out_lo, int64_t out_hi, int32_t* debug_write_count, void* stream) {
+    try {
+        if (!p || !cfg) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, pitches, dm);
+        if (s != AN5D_OK) return s;
+        if ((s = check_alignment(*p, src, dm, "src")) != AN5D_OK) return s;
+        if ((s = check_alignment(*p, dst, dm, "dst")) != AN5D_OK) return s;
+        if (degree < 1 || degree > cfg->bT) return fail(AN5D_ERR_INVALID_ARGUMENT, "degree must be in [1, bT]");
+        if (global_outer_extent < dm.E[0] + outer_offset || outer_offset < 0)
+            return fail(AN5D_ERR_INVALID_ARGUMENT, "slab outside the global array");
+        // clip output planes to the global interior
+        out_lo = std::max(out_lo, (int64_t)p->rad - outer_offset);
+        out_hi = std::min(out_hi, global_outer_extent - p->rad - outer_offset);
+        if (out_lo < 0 || out_hi > dm.E[0]) return fail(AN5D_ERR_INVALID_ARGUMENT, "output planes outside array");
+        if (out_hi <= out_lo) return AN5D_OK;
+        // the inputs the sweep needs must exist locally unless that side is the global face
+        if (out_lo - (int64_t)degree * p->rad < 0 && outer_offset > 0)
+            return fail(AN5D_ERR_INVALID_ARGUMENT, "slab lacks %d ghost planes below", degree * p->rad);
+        if (out_hi + (int64_t)degree * p->rad > dm.E[0] && outer_offset + dm.E[0] < global_outer_extent)
+            return fail(AN5D_ERR_INVALID_ARGUMENT, "slab lacks %d ghost planes above", degree * p->rad);
+        an5d_config c{};
+        if ((s = resolve_config(*p, dm, 0, cfg, c)) != AN5D_OK) return s;
+        if ((s = ensure_streams(*p)) != AN5D_OK) return s;
+        return launch_sweep(*p, src, dst, dm, degree, c, outer_offset, global_outer_extent, out_lo, out_hi,
+                            debug_write_count, (cudaStream_t)stream);
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t* extents, const int64_t* pitches,
+                     int64_t T, const an5d_config* cfg, void* stream) {
+    try {
+        if (!p) return fail(AN5D_ERR_INVALID_ARGUMENT, "plan is NULL");
+        if (T < 0) return fail(AN5D_ERR_INVALID_ARGUMENT, "T < 0");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, pitches, dm);
+        if (s != AN5D_OK) return s;
+        if ((s = check_alignment(*p, grid_in, dm, "grid_in")) != AN5D_OK) return s;
+        if ((s = check_alignment(*p, grid_out, dm, "grid_out")) != AN5D_OK) return s;
+        if (grid_in == grid_out) return fail(AN5D_ERR_INVALID_ARGUMENT, "grid_in and grid_out must differ");
+        cudaStream_t st = (cudaStream_t)stream;
+        p->launches = 0;
+        if (T == 0) return launch_copy(*p, grid_in, grid_out, dm, false, 0, dm.E[0], st);
+        an5d_config c{};
+        if ((s = resolve_config(*p, dm, T, cfg, c)) != AN5D_OK) return s;
+        std::vector<int> deg;
+        bool tc = false;
+        make_schedule(T, c.bT, deg, tc);
+        // validate every sweep's geometry before the first launch (no partial writes on error)
+        for (int d : deg) {
+            const Instance* inst = find_instance(*p, d, c.vec);
+            SweepGeom g{};
+            if ((s = sweep_geometry(*p, *inst, dm, d, c.h, 0, dm.E[0], p->rad, dm.E[0] - p->rad, g)) != AN5D_OK)
+                return s;
+        }
+        if ((s = ensure_streams(*p)) != AN5D_OK) return s;
+        // both buffers carry the input ring (D1: the ring is never written by a sweep)
+        if ((s = launch_copy(*p, grid_in, grid_out, dm, true, 0, dm.E[0], st)) != AN5D_OK) return s;
+        void* bufs[2] = {grid_in, grid_out};
+        for (size_t i = 0; i < deg.size(); ++i) {
+            const void* src = bufs[i % 2];
+            void* dst = bufs[(i + 1) % 2];
+            if ((s = launch_sweep(*p, src, dst, dm, deg[i], c, 0, dm.E[0], p->rad, dm.E[0] - p->rad, nullptr, st)) !=
+                AN5D_OK)
+                return s;
+        }
+        if (tc) {
+            if ((s = launch_copy(*p, grid_in, grid_out, dm, false, 0, dm.E[0], st)) != AN5D_OK) return s;
+        }
+        return AN5D_OK;
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+}  // extern "C"

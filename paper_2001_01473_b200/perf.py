@@ -1,0 +1,67 @@
+"""Performance accounting used by bench.py: FLOP/cell, eff_ALU and the b_T-adjusted roofline.
+
+Pure host arithmetic on counts (no cell data).  Citations:
+  * FLOP/cell: PAPER.md Table 2, with the FMA-merging rule of P:589-605 (k products ->
+    k-1 FMA + 1 MUL; the j-stencil division becomes one MUL under fast math).
+  * eff_ALU: P:611-614.
+  * roofline: BASELINE.json metric "min(FMA peak, HBM BW x bT / bytes-per-cell-per-step),
+    accounting for halo redundancy", written out in SURVEY.md §8(d).
+"""
+from __future__ import annotations
+
+STAR, BOX = 0, 1
+
+
+def n_taps(ndim: int, rad: int, shape: int) -> int:
+    return (2 * rad + 1) ** ndim if shape == BOX else 2 * ndim * rad + 1
+
+
+def flops_per_cell(ndim: int, rad: int, shape: int, has_div: bool) -> int:
+    """Table 2: k products summed = k FMA-equivalent ops counted as 2k-1 FLOPs, +1 for /c_0."""
+    return 2 * n_taps(ndim, rad, shape) - 1 + (1 if has_div else 0)
+
+
+def op_mix(ndim: int, rad: int, shape: int, has_div: bool):
+    """(n_FMA, n_MUL, n_ADD) per cell under the paper's mapping."""
+    k = n_taps(ndim, rad, shape)
+    return k - 1, 1 + (1 if has_div else 0), 0
+
+
+def eff_alu(ndim: int, rad: int, shape: int, has_div: bool) -> float:
+    """eff_ALU = (2 FMA + MUL + ADD + OTHER) / (2 (FMA + MUL + ADD + OTHER))."""
+    f, m, a = op_mix(ndim, rad, shape, has_div)
+    return (2 * f + m + a) / (2 * (f + m + a))
+
+
+def fp_peak_flops(dtype_bytes: int, n_sm: int = 148, clock_mhz: float = 1965.0) -> float:
+    """CUDA-core FMA peak (FLOP/s) from unit counts and clock:
+    B200 SM = 4 SMSPs x 32 FP32 lanes = 128 FFMA/clk; 64 FP64 lanes (DFMA) per SM."""
+    lanes = 128 if dtype_bytes == 4 else 64
+    return n_sm * lanes * 2.0 * clock_mhz * 1e6
+
+
+def roofline(*, ndim, rad, shape, has_div, dtype_bytes, bT, tile_loaded, tile_compute, h, hbm_gbs,
+             fp_peak, rcomp_levels=None):
+    """b_T-adjusted roofline in cells/s for a configuration.
+
+    R_read = (prod loaded / prod compute) * (h + 2 bT rad) / h  -- halo + stream-overlap reloads;
+    R_comp = the same redundancy for the computation (this build's kernels compute the full loaded
+    tile at every level, so R_comp = R_read unless `rcomp_levels` says otherwise).
+    roof = min(P eff_ALU / (F R_comp), B bT / (n_w (R_read + 1))); ideal has R = 1.
+    """
+    import math
+    F = flops_per_cell(ndim, rad, shape, has_div)
+    eff = eff_alu(ndim, rad, shape, has_div)
+    ratio = math.prod(tile_loaded) / math.prod(tile_compute)
+    r_read = ratio * (h + 2 * bT * rad) / h
+    r_comp = r_read if rcomp_levels is None else rcomp_levels
+    comp = fp_peak * eff / (F * r_comp)
+    mem = hbm_gbs * 1e9 * bT / (dtype_bytes * (r_read + 1.0))
+    ideal_comp = fp_peak * eff / F
+    ideal_mem = hbm_gbs * 1e9 * bT / (2.0 * dtype_bytes)
+    return {
+        "roof_cells_s": min(comp, mem), "bound": "alu" if comp < mem else "hbm",
+        "comp_cells_s": comp, "hbm_cells_s": mem, "R_read": r_read, "R_comp": r_comp,
+        "ideal_cells_s": min(ideal_comp, ideal_mem), "flops_per_cell": F, "eff_alu": eff,
+        "alg_bytes_per_cell_step": dtype_bytes * (r_read + 1.0) / bT,
+    }

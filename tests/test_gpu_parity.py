@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Acceptance (BASELINE.json north_star): relative L-inf (normwise, over the interior, SURVEY C-11)
+<= 1e-5 for fp32 and <= 1e-12 for fp64; the ring compared bit-exactly; blocking bookkeeping
+bit-exact -- checked by (i) exact-integer mode (+-1 taps, inputs in {-1,0,1}, T capped so every
+partial sum is an exactly representable integer: any order of summation gives the same bits, so
+GPU == oracle bit-for-bit and any halo/index/mask bug shows) and (ii) per-sweep write-count maps
+(every interior cell stored exactly once, ring never).
+"""
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.float64: 1e-12}
+NP = {torch.float32: np.float32, torch.float64: np.float64}
+
+
+def rel_linf(got, exp, rad):
+    core = tuple(slice(rad, e - rad) for e in exp.shape)
+    den = np.abs(exp[core]).max()
+    return np.abs(got[core].astype(np.float64) - exp[core].astype(np.float64)).max() / max(den, 1e-300)
+
+
+def ring_equal(got, exp, rad):
+    mask = np.ones(exp.shape, bool)
+    mask[tuple(slice(rad, e - rad) for e in exp.shape)] = False
+    return np.array_equal(got[mask], exp[mask])
+
+
+def gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg=None):
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    b = an5d.empty_grid(g.shape, rad, dtype)
+    b.fill_(float("nan"))
+    st.run(a, b, T, cfg)
+    torch.cuda.synchronize()
+    return b.cpu().numpy(), st
+
+
+def small_ext(ndim, rad):
+    # spans several tiles in every blocked dim (2D tiles 128..256 wide, 3D 64 x 16..64) + ragged tails
+    return (61 + 2 * rad, 411 + 2 * rad) if ndim == 2 else (23 + 2 * rad, 83 + 2 * rad, 141 + 2 * rad)
+
+
+def configs_for(an5d, st, ext, ndim):
+    """A spread of available (bT, vec) configurations for this stencil, with short stream blocks so
+    several stream blocks (and interior + edge launches) are exercised."""
+    out = []
+    for vec in (1, 2, 4, 8):
+        bts = []
+        for bT in range(1, 11):
+            try:
+                st.describe(ext, {"bT": bT, "vec": vec, "h": 16})
+                bts.append(bT)
+            except an5d.AN5DError:
+                pass
+        if bts:
+            picks = sorted({bts[0], bts[len(bts) // 2], bts[-1]})
+            out += [{"bT": b, "vec": vec, "h": 16 if ndim == 2 else 8} for b in picks]
+    return out
+
+
+BENCH = sorted(inputs.BENCHMARKS)
+
+
+@pytest.mark.parametrize("name", BENCH)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_random_parity_all_configs(an5d, name, dtype):
+    """Uniform [0,1) inputs, dyadic (or j-stencil integer/divisor) coefficients; every instance
+    family; T in {1, bT, bT+1, 2bT+3}."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    cfgs = configs_for(an5d, st, ext, ndim)
+    assert cfgs, f"no kernel instance for {name}"
+    for cfg in cfgs:
+        bT = cfg["bT"]
+        for T in sorted({1, bT, bT + 1, 2 * bT + 3}):
+            got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+            exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+            assert ring_equal(got, exp, rad), (cfg, T)
+            err = rel_linf(got, exp, rad)
+            assert err <= TOL[dtype], (name, cfg, T, err)
+
+
+def _exact_T(ndim, rad, shape, T_want, dtype):
+    taps = (2 * rad + 1) ** ndim if shape == inputs.BOX else 2 * ndim * rad + 1
+    lim = 2.0 ** (24 if dtype == torch.float32 else 53)
+    T = 0
+    bound = 1.0
+    while T < T_want and bound * taps < lim:
+        bound *= taps
+        T += 1
+    return T
+
+
+@pytest.mark.parametrize("name", BENCH)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_exact_integer_bit_identical(an5d, name, dtype):
+    """+-1 taps, inputs in {-1,0,1}: every partial sum is an exact integer (< 2^24 / 2^53), so the
+    GPU result must equal the oracle bit-for-bit whatever the summation order -- pins tile/halo
+    indices, boundary masks and the sweep schedule exactly."""
+    ndim, rad, shape, _, _ = inputs.benchmark_problem(name)
+    tab, div = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(1234, ext, kind="pm")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    for cfg in configs_for(an5d, st, ext, ndim):
+        T = _exact_T(ndim, rad, shape, 2 * cfg["bT"] + 3, dtype)
+        if T < 1:
+            continue
+        got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+        exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+        assert np.array_equal(got, exp), (name, cfg, T)
+
+
+@pytest.mark.parametrize("name", ["star2d1r", "box2d3r", "j2d9pt", "star3d2r", "box3d1r", "box3d4r"])
+def test_write_count_map(an5d, name):
+    """One sweep: every interior cell stored exactly once, ring cells never (S:213 coverage and
+    disjointness of compute regions)."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    g = inputs.global_grid(5, ext)
+    a = an5d.to_grid(torch.from_numpy(g.astype(np.float32)).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, torch.float32)
+    for cfg in configs_for(an5d, st, ext, ndim):
+        wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+        st.copy_ring(a, b)
+        st.sweep(a, b, cfg["bT"], cfg, write_count=wc)
+        torch.cuda.synchronize()
+        w = wc.cpu().numpy()
+        core = tuple(slice(rad, e - rad) for e in ext)
+        assert np.all(w[core] == 1), cfg
+        w[core] = 0
+        assert not w.any(), cfg
+
+
+def test_baseline_config1_full(an5d):
+    """BASELINE config 1: star2d1r fp32 512^2, T=100, bT=4 -- full grid against the oracle."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("star2d1r")
+    ext = (512 + 2, 512 + 2)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    got, st = gpu_run(an5d, ndim, rad, shape, tab, div, g, 100, torch.float32, {"bT": 4})
+    exp = oracle.run(g, rad, shape, tab, div, 100, np.float32)
+    assert ring_equal(got, exp, rad)
+    assert rel_linf(got, exp, rad) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_edge_cases(an5d, dtype):
+    """Degenerate sizes: a single interior cell, interior smaller than one tile, one interior plane,
+    T = 0, T < bT."""
+    for ndim, rad, shape in [(2, 1, inputs.STAR), (2, 3, inputs.BOX), (3, 1, inputs.BOX), (3, 2, inputs.STAR)]:
+        tab, div = inputs.coeff_table(ndim, rad, shape, seed=4)
+        for n in ([1, 1], [3, 5], [1, 40]) if ndim == 2 else ([1, 1, 1], [2, 3, 5], [9, 1, 70]):
+            ext = tuple(v + 2 * rad for v in n)
+            g = inputs.global_grid(8, ext)
+            for T in (0, 1, 2, 5):
+                got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype)
+                exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+                assert ring_equal(got, exp, rad)
+                assert rel_linf(got, exp, rad) <= TOL[dtype], (ndim, rad, n, T)
+
+
+def test_errors_before_launch(an5d):
+    """Misaligned pitch / base -> AN5D_ERR_UNSUPPORTED with nothing written."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("star2d1r")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    a = torch.zeros(10, 13, device="cuda")          # pitch 13 floats: not 16-byte multiple
+    b = torch.full((10, 13), 7.0, device="cuda")
+    with pytest.raises(an5d.AN5DError) as e:
+        st.run(a, b, 3)
+    assert e.value.status == 5
+    assert torch.all(b == 7.0)
+
+
+def test_run_split_equals_single_run(an5d):
+    """Checkpoint/resume semantics: run(T1) then run(T2) == run(T1+T2) bit-exactly when the sweep
+    degrees coincide (both schedules are all-bT sweeps here)."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("box2d1r")
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(3, ext)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    cfg = {"bT": 3, "vec": 4, "h": 32}
+    a = an5d.to_grid(torch.from_numpy(g.astype(np.float32)).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, torch.float32)
+    st.run(a, b, 9, cfg)                      # 3 sweeps of 3 -> result in b
+    full = b.clone()
+    a2 = an5d.to_grid(torch.from_numpy(g.astype(np.float32)).cuda(), rad)
+    b2 = an5d.empty_grid(ext, rad, torch.float32)
+    st.run(a2, b2, 3, cfg)
+    a3 = an5d.to_grid(b2, rad)
+    b3 = an5d.empty_grid(ext, rad, torch.float32)
+    st.run(a3, b3, 6, cfg)                    # schedule [3, 3] is even -> split: [3, 2, 1]
+    torch.cuda.synchronize()
+    err = rel_linf(b3.cpu().numpy(), full.cpu().numpy(), rad)
+    assert err <= 1e-6

@@ -1,0 +1,150 @@
+"""Host-side logic without a GPU: C-ABI exports, bit-exact bookkeeping, schedule, FLOP accounting."""
+import json
+import math
+import os
+import re
+
+import pytest
+
+import oracle.geometry as og
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def test_library_loads_and_exports_every_declared_symbol(an5d):
+    """Every function declared in include/an5d.h is exported by libAN5D.so."""
+    import ctypes
+    hdr = open(os.path.join(REPO, "include", "an5d.h")).read()
+    declared = set(re.findall(r"^\s*(?:an5d_status|const char\*|int64_t)\s+(an5d_\w+)\s*\(", hdr, re.M))
+    assert {"an5d_create", "an5d_run", "an5d_destroy", "an5d_sweep", "an5d_describe"} <= declared
+    lib = ctypes.CDLL(an5d.LIB_PATH)
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert set(an5d.EXPORTED_SYMBOLS) == declared
+    assert "sm_100a" in an5d.version()
+
+
+def test_oracle_geometry_spec_examples():
+    """The paper's formulas (oracle.geometry) reproduce SPEC.md's worked examples."""
+    ex = _gold("spec_geometry.json")["examples"]
+    e = ex[0]
+    assert og.n_thr(e["bS"]) == e["n_thr"]
+    assert [og.compute_region(b, e["bT"], e["rad"]) for b in e["bS"]] == e["compute_region"]
+    ntb = og.n_tb(e["I_S"][1:], e["bS"], e["bT"], e["rad"])
+    assert ntb == e["n_tb"]
+    assert og.n_tb_prime(e["I_S"][0], e["h_SN"], ntb) == e["n_tb_prime"]
+    assert og.stream_overlap(e["bT"], e["rad"]) == e["stream_overlap"]
+    e = ex[1]
+    assert og.compute_region(e["bS"][0], e["bT"], e["rad"]) == e["compute_region"][0]
+    assert og.n_tb(e["I_S"], e["bS"], e["bT"], e["rad"]) == e["n_tb"]
+    e = ex[2]
+    assert og.compute_region(e["bS"][0], e["bT"], e["rad"]) < 1
+
+
+def test_stream_overlap_closed_form():
+    """2 sum_{T<bT} rad (bT - T) == rad bT (bT + 1)."""
+    for bT in range(1, 17):
+        for rad in range(1, 5):
+            assert og.stream_overlap(bT, rad) == rad * bT * (bT + 1)
+
+
+def test_valid_region_recurrence():
+    for bS in (16, 64, 256):
+        for rad in (1, 2):
+            for T in range(0, 5):
+                assert og.valid_region(bS, T + 1, rad) == og.valid_region(bS, T, rad) - 2 * rad
+
+
+@pytest.mark.parametrize("case", _gold("schedule_survey.json")["cases"])
+def test_schedule_matches_survey_table(case, an5d):
+    """Library (C++) and oracle (Python) schedules equal SURVEY's independently computed table."""
+    exp = [d for d, n in case["degrees"] for _ in range(n)]
+    deg, copy = og.schedule(case["T"], case["bT"])
+    assert deg == exp and copy == case["copy"]
+    deg2, copy2 = an5d.schedule(case["T"], case["bT"])
+    assert deg2 == exp and copy2 == case["copy"]
+
+
+def test_schedule_invariants(an5d):
+    for T in range(0, 60):
+        for bT in range(1, 11):
+            deg, copy = an5d.schedule(T, bT)
+            assert (deg, copy) == og.schedule(T, bT)
+            assert sum(deg) == T
+            assert all(1 <= d <= bT for d in deg)
+            if T > 0:
+                assert (len(deg) % 2 == 1) or copy
+                assert not (copy and len(deg) % 2 == 1)
+            # the paper's literal condition never misses a case that needs adjusting
+            if T % bT != 0:
+                assert og.paper_adjustment_condition(T, bT)
+
+
+@pytest.mark.parametrize("name", ["star2d1r", "box2d2r", "j2d5pt", "star3d1r", "box3d1r", "star3d4r", "j3d27pt",
+                                  "box2d4r", "star2d4r"])
+@pytest.mark.parametrize("dtype_name", ["float32", "float64"])
+def test_describe_matches_paper_formulas(name, dtype_name, an5d):
+    """an5d_describe (C++) is bit-exact with the paper's formulas (oracle.geometry) for every
+    configuration the library exposes."""
+    import torch
+
+    import inputs
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    dtype = getattr(torch, dtype_name)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    ext = [16384 + 2 * rad] * 2 if ndim == 2 else [512 + 2 * rad] * 3
+    n = 0
+    for bT in range(1, 11):
+        for vec in (1, 2, 4, 8):
+            for h in (128, 500, 4096):
+                try:
+                    g = st.describe(ext, {"bT": bT, "vec": vec, "h": h})
+                except an5d.AN5DError as e:
+                    assert e.status in (2, 5)   # infeasible / no instance
+                    continue
+                n += 1
+                nb = ndim - 1
+                I_S = [e - 2 * rad for e in ext]
+                bS = g["bS"][:nb]
+                assert g["compute"][:nb] == [og.compute_region(b, bT, rad) for b in bS]
+                assert g["n_tiles"][:nb] == [math.ceil(I / c) for I, c in zip(I_S[1:], g["compute"][:nb])]
+                assert g["n_tb"] == og.n_tb(I_S[1:], bS, bT, rad)
+                assert g["n_tb_prime"] == og.n_tb_prime(I_S[0], g["h"], g["n_tb"])
+                assert g["stream_overlap"] == og.stream_overlap(bT, rad)
+                assert all(hl >= bT * rad for hl in g["halo_loaded"][:nb])
+                assert all(bl == c + 2 * hl for bl, c, hl in zip(g["bS_loaded"][:nb], g["compute"][:nb],
+                                                                  g["halo_loaded"][:nb]))
+    assert n > 0
+
+
+def test_create_rejects_bad_arguments(an5d):
+    import numpy as np
+    import torch
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.Stencil(2, 1, an5d.STAR, np.ones((3, 3)), 1.0, torch.float32)   # off-axis non-zero
+    assert e.value.status == 4
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.Stencil(2, 5, an5d.BOX, np.ones((11, 11)), 1.0, torch.float32)
+    assert e.value.status == 1
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.Stencil(4, 1, an5d.BOX, np.ones((3, 3, 3, 3)), 1.0, torch.float32)
+    assert e.value.status == 1
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.Stencil(2, 1, an5d.BOX, np.ones((3, 3)), 0.0, torch.float32)
+    assert e.value.status == 1
+
+
+def test_flops_per_cell_table2():
+    from paper_2001_01473_b200 import perf
+    import inputs
+    g = _gold("table2_flops.json")["flops"]
+    for name, (ndim, rad, shape, has_div) in inputs.BENCHMARKS.items():
+        assert perf.flops_per_cell(ndim, rad, shape, has_div) == g[name], name
+    # eff_ALU for star2d1r: 4 FMA + 1 MUL -> 9/10
+    assert abs(perf.eff_alu(2, 1, 0, False) - 0.9) < 1e-15
