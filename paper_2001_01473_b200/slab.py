@@ -1,0 +1,308 @@
+"""Slab decomposition of the streaming dimension across GPUs (BASELINE north_star (d)).
+
+The paper is single-GPU; its "division of the streaming dimension" into stream blocks
+is the geometry reused here: rank k owns a contiguous run of interior planes of the OUTERMOST
+(streaming) dimension and holds G = b_T * rad ghost planes on each side that has a neighbour.
+Every sweep of degree d:
+
+  1. the BOUNDARY output planes (the lowest / highest owned planes a neighbour needs next sweep)
+     are computed first, on the caller's stream;
+  2. their outermost d_next * rad planes are exchanged with rank-1 / rank+1 (send owned planes,
+     receive into ghost planes of the same destination buffer) on a separate comm stream;
+  3. the INTERIOR output planes are computed on the caller's stream while the exchange runs;
+  4. the next sweep waits for both.
+
+Bookkeeping (:class:`SlabPlan`) is pure integer host logic, shared by the NCCL runner
+(:func:`run_distributed`, one process per GPU), the in-process loopback runner used for single-GPU
+tests (:func:`run_loopback`) and the world-size-2 gloo CPU tests.  The compute itself is the
+library's ``an5d_sweep`` in slab mode (outer_offset / global_outer_extent, include/an5d.h); the
+exchange is torch.distributed send/recv (NCCL over NVLink on the GPU box).
+"""
+from __future__ import annotations
+
+import dataclasses
+import json
+import os
+import statistics
+import time
+
+
+@dataclasses.dataclass(frozen=True)
+class Slab:
+    rank: int
+    nranks: int
+    gE0: int          # global outermost extent (ring planes included)
+    rad: int
+    G: int            # ghost depth (planes) = b_T * rad
+    own_lo: int       # owned global interior planes [own_lo, own_hi)
+    own_hi: int
+    loc_lo: int       # global planes held locally [loc_lo, loc_hi) (owned + ghosts / global ring)
+    loc_hi: int
+
+    @property
+    def n_local(self) -> int:
+        return self.loc_hi - self.loc_lo
+
+    @property
+    def out_lo(self) -> int:      # owned planes in local coordinates
+        return self.own_lo - self.loc_lo
+
+    @property
+    def out_hi(self) -> int:
+        return self.own_hi - self.loc_lo
+
+    @property
+    def has_lower(self) -> bool:
+        return self.rank > 0
+
+    @property
+    def has_upper(self) -> bool:
+        return self.rank < self.nranks - 1
+
+
+def partition(gE0: int, rad: int, nranks: int, G: int, align: int = 1):
+    """Contiguous owned chunks of the global interior planes [rad, gE0 - rad).
+
+    chunk = ceil(I / n) rounded up to a multiple of ``align`` (the stream-block length, so slabs
+    add no redundancy beyond the single-GPU stream overlap); every rank must own at
+    least G planes (a ghost region never spans two ranks).
+    """
+    I = gE0 - 2 * rad
+    if nranks < 1 or I < nranks:
+        raise ValueError(f"cannot split {I} interior planes over {nranks} ranks")
+    chunk = -(-I // nranks)
+    chunk = -(-chunk // align) * align
+    out = []
+    for k in range(nranks):
+        lo = rad + min(I, k * chunk)
+        hi = rad + min(I, (k + 1) * chunk)
+        if hi - lo < G and nranks > 1:
+            raise ValueError(f"rank {k} owns {hi - lo} planes < ghost depth {G}; use fewer ranks")
+        out.append(Slab(k, nranks, gE0, rad, G, lo, hi, max(0, lo - G), min(gE0, hi + G)))
+    return out
+
+
+@dataclasses.dataclass(frozen=True)
+class SweepParts:
+    """Output-plane ranges (local coordinates) of one sweep on one slab."""
+    boundary: tuple   # ranges computed before the exchange
+    interior: tuple   # ranges computed concurrently with the exchange
+    sends: tuple      # (peer, local_lo, n_planes): owned planes sent to peer
+    recvs: tuple      # (peer, local_lo, n_planes): ghost planes received from peer
+
+
+def sweep_parts(s: Slab, next_degree: int, h: int) -> SweepParts:
+    """Split the owned planes of a sweep into boundary and interior parts and list the exchange
+    for a following sweep of degree ``next_degree`` (0 = none): it needs next_degree * rad ghost
+    planes per neighbour side."""
+    g = next_degree * s.rad
+    lo, hi = s.out_lo, s.out_hi
+    hb = max(g, h)
+    blo = lo + hb if (s.has_lower and g) else lo          # [lo, blo) boundary below
+    bhi = hi - hb if (s.has_upper and g) else hi          # [bhi, hi) boundary above
+    if blo >= bhi:                                        # slab too thin to overlap
+        boundary, interior = ((lo, hi),), ()
+    else:
+        boundary = tuple(r for r in ((lo, blo), (bhi, hi)) if r[1] > r[0])
+        interior = ((blo, bhi),)
+    sends, recvs = [], []
+    if g:
+        if s.has_lower:
+            sends.append((s.rank - 1, lo, g))
+            recvs.append((s.rank - 1, lo - g, g))
+        if s.has_upper:
+            sends.append((s.rank + 1, hi - g, g))
+            recvs.append((s.rank + 1, hi, g))
+    return SweepParts(boundary, interior, tuple(sends), tuple(recvs))
+
+
+def local_extents(s: Slab, inner_extents):
+    return (s.n_local,) + tuple(int(e) for e in inner_extents)
+
+
+# ---------------------------------------------------------------------------------------------
+# Runners
+# ---------------------------------------------------------------------------------------------
+def _plane_view(buf, lo, n):
+    """Contiguous flat view of local planes [lo, lo + n) of a (possibly padded) grid view."""
+    import torch
+    pz = buf.stride(0)
+    flat = torch.empty(0, dtype=buf.dtype, device=buf.device).set_(buf.untyped_storage())
+    start = buf.storage_offset() + lo * pz
+    return flat[start:start + n * pz]
+
+
+def run_distributed(stencil, s: Slab, bufs, T: int, cfg: dict, group=None, comm_stream=None,
+                    schedule_fn=None):
+    """One rank's share of a T-step run (torch.distributed already initialised; NCCL on GPUs).
+
+    ``bufs`` = (grid_in, grid_out) local slab arrays (ghosts included), grid_in holding the input
+    on every local plane.  On return grid_out's owned planes hold step T.  ``stencil`` is a
+    :class:`paper_2001_01473_b200.Stencil` (or any object with the same sweep/copy_ring API).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import schedule as lib_schedule
+    degrees, trailing = (schedule_fn or lib_schedule)(T, cfg["bT"])
+    a, b = bufs
+    main = torch.cuda.current_stream() if a.is_cuda else None
+    comm = comm_stream if comm_stream is not None else (torch.cuda.Stream(a.device) if a.is_cuda else None)
+    gE0 = s.gE0
+    stencil.copy_ring(a, b, outer_offset=s.loc_lo, global_outer_extent=gE0)
+    ev_prev = None
+    for i, d in enumerate(degrees):
+        src, dst = (a, b) if i % 2 == 0 else (b, a)
+        nd = degrees[i + 1] if i + 1 < len(degrees) else 0
+        parts = sweep_parts(s, nd, int(cfg.get("h") or 0))
+        if ev_prev is not None and main is not None:
+            main.wait_event(ev_prev)
+        for lo, hi in parts.boundary:
+            stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=gE0, out_lo=lo, out_hi=hi)
+        if parts.sends or parts.recvs:
+            if main is not None:
+                ev_b = torch.cuda.Event()
+                ev_b.record(main)
+                with torch.cuda.stream(comm):
+                    comm.wait_event(ev_b)
+                    _exchange(dst, parts, group)
+                    ev_prev = torch.cuda.Event()
+                    ev_prev.record(comm)
+            else:
+                _exchange(dst, parts, group)
+        for lo, hi in parts.interior:
+            stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=gE0, out_lo=lo, out_hi=hi)
+    if ev_prev is not None and main is not None:
+        main.wait_event(ev_prev)
+    if trailing:
+        # b_T == 1 with an even sweep count: the result sits in grid_in; copy the owned planes
+        n = s.out_hi - s.out_lo
+        _plane_view(b, s.out_lo, n).copy_(_plane_view(a, s.out_lo, n))
+    return b
+
+
+def _exchange(dst, parts: SweepParts, group):
+    import torch.distributed as dist
+    ops = []
+    for peer, lo, n in parts.recvs:
+        ops.append(dist.P2POp(dist.irecv, _plane_view(dst, lo, n), peer, group))
+    for peer, lo, n in parts.sends:
+        ops.append(dist.P2POp(dist.isend, _plane_view(dst, lo, n).contiguous(), peer, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def run_loopback(stencil, slabs, bufs_per_slab, T: int, cfg: dict, schedule_fn=None):
+    """All slabs in one process on one device, ghost planes exchanged by device copies: the same
+    partition, sweep split and slab-mode sweeps as :func:`run_distributed` (single-GPU CI of the
+    multi-GPU bookkeeping, SURVEY.md §4 "loopback mode")."""
+    from . import schedule as lib_schedule
+    degrees, trailing = (schedule_fn or lib_schedule)(T, cfg["bT"])
+    for s, (a, b) in zip(slabs, bufs_per_slab):
+        stencil.copy_ring(a, b, outer_offset=s.loc_lo, global_outer_extent=s.gE0)
+    for i, d in enumerate(degrees):
+        nd = degrees[i + 1] if i + 1 < len(degrees) else 0
+        plist = []
+        for s, (a, b) in zip(slabs, bufs_per_slab):
+            src, dst = (a, b) if i % 2 == 0 else (b, a)
+            parts = sweep_parts(s, nd, int(cfg.get("h") or 0))
+            plist.append((parts, dst))
+            for lo, hi in parts.boundary + parts.interior:
+                stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=s.gE0,
+                              out_lo=lo, out_hi=hi)
+        for k, (parts, dst) in enumerate(plist):
+            for peer, lo, n in parts.recvs:
+                ppart, pdst = plist[peer]
+                # the peer's matching send: same length, the side facing rank k
+                (sl,) = [x for x in ppart.sends if x[0] == k]
+                _plane_view(dst, lo, n).copy_(_plane_view(pdst, sl[1], n))
+    if trailing:
+        for s, (a, b) in zip(slabs, bufs_per_slab):
+            n = s.out_hi - s.out_lo
+            _plane_view(b, s.out_lo, n).copy_(_plane_view(a, s.out_lo, n))
+    return [b for _, b in bufs_per_slab]
+
+
+# ---------------------------------------------------------------------------------------------
+# bench.py --gpus N (N > 1): one process per GPU under torchrun
+# ---------------------------------------------------------------------------------------------
+def bench_main(args, workloads):
+    """Strong-scaling bench of one workload over N GPUs (see bench.py); rank 0 prints the line."""
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import paper_2001_01473_b200 as an5d
+    from paper_2001_01473_b200 import perf
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    name, dtype_name, n, T = workloads[args.workload]
+    if args.T:
+        T = args.T
+    dtype = getattr(torch, dtype_name)
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    gext = (n + 2 * rad,) * ndim
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    # the planner picks (bT, vec, h) for this rank's slab shape
+    probe = (-(-n // ws) + 2 * rad,) + gext[1:]
+    cfg = st.plan_config(probe, T, {"bT": args.bt, "vec": args.vec, "h": args.h})
+    slabs = partition(gext[0], rad, ws, cfg["bT"] * rad, align=1)
+    s = slabs[rank]
+    lext = local_extents(s, gext[1:])
+    a = an5d.empty_grid(lext, rad, dtype, dev)
+    b = an5d.empty_grid(lext, rad, dtype, dev)
+    from bench import fill_uniform, ClockSampler, _peaks
+    fill_uniform(a, inputs.DEFAULT_SEED, gext, outer_offset=s.loc_lo)
+    b.copy_(a)
+    comm = torch.cuda.Stream(dev)
+    bufs = [a, b]
+
+    def step(i):
+        src, dst = bufs[i % 2], bufs[(i + 1) % 2]
+        run_distributed(st, s, (src, dst), T, cfg, comm_stream=comm)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for i in range(args.steps):
+            step(args.warmup + i)
+        ev1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    cells = float(n) ** ndim
+    gcells = cells * T / (ms * 1e-3) / 1e9
+    F = perf.flops_per_cell(ndim, rad, shape, div != 1.0)
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": f"GCells/s ({name} {dtype_name} {n}^{ndim}, T={T})", "value": round(gcells, 3),
+            "unit": "GCells/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if dtype == torch.float32 else "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "stencil": name, "grid": list(gext), "T": T, "bT": cfg["bT"],
+                       "vec": cfg["vec"], "h": cfg["h"], "parallelism": f"slab{ws} (outermost dim, NCCL halo)",
+                       "l2": "inputs larger than L2"},
+            "gflops": round(gcells * F, 2), "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None,
+            "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
