@@ -227,10 +227,39 @@ def main():
     ap.add_argument("--ref-step-seconds", type=float, default=3.0)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--T", type=int, default=0, help="override the time-step count")
+    ap.add_argument("--suite", default="", help="comma list of workload names (or 'all2d', 'all3d', 'all') "
+                    "to run back to back at the planner's config; one JSON line each (not a driver line)")
+    ap.add_argument("--bt-sweep", default="", help="with --suite: comma list of b_T values to force in turn")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.suite:
+        return run_suite(args)
     return run_an5d(args)
+
+
+def run_suite(args):
+    """BASELINE configs 2-3: every Table-2 stencil (fp32 and fp64) at full size, one line each."""
+    sel = []
+    for tok in args.suite.split(","):
+        if tok in ("all", "all2d"):
+            sel += [w for w in WORKLOADS if w.endswith("-16384")]
+        if tok in ("all", "all3d"):
+            sel += [w for w in WORKLOADS if w.endswith("-512")]
+        if tok in WORKLOADS:
+            sel.append(tok)
+    seen = set()
+    sel = [w for w in sel if not (w in seen or seen.add(w))]
+    bts = [int(b) for b in args.bt_sweep.split(",") if b] or [args.bt]
+    for w in sel:
+        for bt in bts:
+            a = argparse.Namespace(**vars(args))
+            a.workload, a.bt, a.no_cpu_baseline, a.no_e2e = w, bt, True, True
+            try:
+                run_an5d(a)
+            except Exception as e:  # report and continue (e.g. no instance for a forced b_T)
+                print(json.dumps({"workload": w, "bT": bt, "error": str(e)[:300]}), flush=True)
+    return 0
 
 
 def run_an5d(args):

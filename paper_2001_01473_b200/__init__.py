@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libAN5D.so")
+LIB_PATH = os.environ.get("AN5D_LIB") or os.path.join(_HERE, "libAN5D.so")
 
 STAR, BOX = 0, 1
 F32, F64 = 0, 1

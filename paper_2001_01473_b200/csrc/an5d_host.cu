@@ -57,7 +57,10 @@ struct Plan {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int device = -1;
     int64_t launches = 0;
+    unsigned long long* ctr = nullptr;  // kCtrRing dynamic-scheduling counter pairs (device, zeroed)
+    int64_t ctr_seq = 0;                // launches that used a counter pair
 };
+constexpr int kCtrRing = 64;            // counter pairs in flight per plan (>= concurrent sweeps)
 
 }  // namespace an5d
 
@@ -278,7 +281,7 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     const double warp_instr = thread_cells * instr_per_cell_level / 32.0;
     const double t_issue = warp_instr / (4.0 * di.n_sm * di.clock_ghz * 1e9);
     // waves
-    const int per_sm = resident_blocks(inst) * (p.ndim == 2 ? kWarps2D : 1);
+    const int per_sm = resident_blocks(inst) * 1;
     const double conc = (double)per_sm * di.n_sm;
     const double waves = (double)g.n_units / conc;
     const double eff = waves / std::ceil(waves);
@@ -310,7 +313,7 @@ an5d_status choose_config(const Plan& p, const Dims& dm, int64_t T, const an5d_c
             if (sweep_geometry(p, inst, dm, inst.bT, Iout, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g) != AN5D_OK) continue;
             int64_t nt = 1;
             for (int i = 0; i < p.ndim - 1; ++i) nt *= g.ntiles[i];
-            const int per_sm = resident_blocks(inst) * (p.ndim == 2 ? kWarps2D : 1);
+            const int per_sm = resident_blocks(inst) * 1;
             const int64_t conc = (int64_t)per_sm * di.n_sm;
             for (int w = 1; w <= 8; ++w) {
                 const int64_t nsb = std::max<int64_t>(1, (w * conc) / std::max<int64_t>(1, nt));
@@ -412,6 +415,9 @@ an5d_status ensure_streams(Plan& p) {
     if ((e = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
     if ((e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
     if ((e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    if (p.ctr) cudaFree(p.ctr);
+    if ((e = cudaMalloc(&p.ctr, sizeof(unsigned long long) * 2 * kCtrRing)) != cudaSuccess) return cuda_fail(e, "counter");
+    if ((e = cudaMemset(p.ctr, 0, sizeof(unsigned long long) * 2 * kCtrRing)) != cudaSuccess) return cuda_fail(e, "counter");
     p.device = dev;
     return AN5D_OK;
 }
@@ -428,28 +434,35 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
     const int64_t n_edge = g.n_units - g.n_interior;
     cudaError_t e;
     if (p.ndim == 2) {
+        // one persistent launch over every (tile, stream block) unit, interior and edge alike
         Sweep2DArgs a{};
         a.src = src; a.dst = dst; a.pitch = dm.pitch[0];
         a.Ey = dm.E[0]; a.g_off = g_off; a.gEy = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
-        a.h = g.h; a.n_sb = g.n_sb; a.sb_lo = g.sb_lo; a.sb_hi = g.sb_hi;
-        a.tx_lo = (int)g.t_lo[0]; a.tx_hi = (int)g.t_hi[0];
+        a.h = g.h; a.n_units = g.n_units; a.n_sb = g.n_sb;
+        a.ctr = p.ctr + 2 * (p.ctr_seq++ % kCtrRing);
         a.wc = wc; a.Ex = (int)dm.E[1]; a.C = g.C[0]; a.H = g.halo[0]; a.n_tiles_x = (int)g.ntiles[0];
-        if (n_edge > 0) {
-            if ((e = cudaEventRecord(p.ev_fork, st)) != cudaSuccess) return cuda_fail(e, "event record");
-            if ((e = cudaStreamWaitEvent(p.side, p.ev_fork, 0)) != cudaSuccess) return cuda_fail(e, "wait");
-            Sweep2DArgs ae = a;
-            ae.n_units = n_edge;
-            if ((e = inst->launch2d(ae, p.coeffs_dev_t.data(), cdiv(n_edge, kWarps2D), true, p.side)) != cudaSuccess)
-                return cuda_fail(e, "edge sweep launch");
-            p.launches++;
-            if ((e = cudaEventRecord(p.ev_join, p.side)) != cudaSuccess) return cuda_fail(e, "event record");
+        const int64_t cap = (int64_t)resident_blocks(*inst) * dev_info().n_sm;
+        const int64_t blocks = std::min<int64_t>(g.n_units, cap);
+        // AN5D_UNIT_PROFILE=path: debug-only per-unit timing dump (synchronises; never in benches)
+        const char* prof_path = getenv("AN5D_UNIT_PROFILE");
+        if (prof_path && !wc) cudaMalloc(&a.unit_ns, sizeof(long long) * 3 * g.n_units);
+        if ((e = inst->launch2d(a, p.coeffs_dev_t.data(), blocks, false, st)) != cudaSuccess)
+            return cuda_fail(e, "sweep launch");
+        p.launches++;
+        if (a.unit_ns) {
+            std::vector<long long> h(3 * g.n_units);
+            cudaStreamSynchronize(st);
+            cudaMemcpy(h.data(), a.unit_ns, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+            cudaFree(a.unit_ns);
+            if (FILE* f = fopen(prof_path, "a")) {
+                fprintf(f, "# sweep degree %d n_units %lld ntx %lld h %lld blocks %lld\n", d, (long long)g.n_units,
+                        (long long)g.ntiles[0], (long long)g.h, (long long)blocks);
+                for (int64_t u = 0; u < g.n_units; ++u)
+                    fprintf(f, "%lld %lld %lld %lld\n", (long long)u, h[3 * u], h[3 * u + 1], h[3 * u + 2]);
+                fclose(f);
+            }
         }
-        if (g.n_interior > 0) {
-            a.n_units = g.n_interior;
-            if ((e = inst->launch2d(a, p.coeffs_dev_t.data(), cdiv(g.n_interior, kWarps2D), false, st)) != cudaSuccess)
-                return cuda_fail(e, "interior sweep launch");
-            p.launches++;
-        }
+        return AN5D_OK;
     } else {
         Sweep3DArgs a{};
         a.src = src; a.dst = dst; a.pz = dm.pitch[0]; a.py = dm.pitch[1];
@@ -618,6 +631,7 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
 
 an5d_status an5d_destroy(an5d_plan* p) {
     if (!p) return AN5D_OK;
+    if (p->ctr) cudaFree(p->ctr);
     if (p->side) {
         cudaStreamDestroy(p->side);
         cudaEventDestroy(p->ev_fork);
@@ -690,8 +704,9 @@ an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_confi
         for (int T = 0; T < c.bT; ++T) ov += (int64_t)p->rad * (c.bT - T);
         out->stream_overlap = 2 * ov;
         out->n_thr = inst->threads;
-        out->units_per_block = p->ndim == 2 ? kWarps2D : 1;
-        out->grid_blocks = p->ndim == 2 ? cdiv(g.n_interior, kWarps2D) + cdiv(g.n_units - g.n_interior, kWarps2D)
+        out->units_per_block = 1;
+        out->grid_blocks = p->ndim == 2 ? std::min<int64_t>(g.n_units,
+                                                            (int64_t)resident_blocks(*inst) * dev_info().n_sm)
                                         : g.n_units;
         out->smem_bytes = inst->smem_bytes;
         cudaFuncAttributes attr{};

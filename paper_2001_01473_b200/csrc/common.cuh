@@ -85,6 +85,20 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, int src
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
                  "r"(src_bytes));
 }
+// Predicated 16-byte copy (no branch: the predicate guards the instruction itself).
+__device__ __forceinline__ void cp_async16_pred(void* sdst, const void* gsrc, int src_bytes, bool pred) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
+                 " @p cp.async.cg.shared.global [%0], [%1], 16, %2;\n}\n" ::"r"(smem_u32(sdst)), "l"(gsrc),
+                 "r"(src_bytes), "r"((int)pred));
+}
+// Predicated element-sized copy (4 or 8 bytes, .ca) with zero-fill: src_bytes is 0 or N.
+template <int N>
+__device__ __forceinline__ void cp_async_elem_pred(void* sdst, const void* gsrc, int src_bytes, bool pred) {
+    static_assert(N == 4 || N == 8, "cp.async.ca element size");
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                 " @p cp.async.ca.shared.global [%0], [%1], %2, %3;\n}\n" ::"r"(smem_u32(sdst)), "l"(gsrc), "n"(N),
+                 "r"(src_bytes), "r"((int)pred));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

@@ -37,13 +37,15 @@ struct Registrar {
 };
 
 template <typename T, int R, int BT, int V, bool BOX>
-cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, bool edge,
+cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, bool /*edge*/,
                      cudaStream_t st) {
     Coeffs<T, (2 * R + 1) * (2 * R + 1)> cf;
     const T* c = static_cast<const T*>(coeffs);
     for (int i = 0; i < (2 * R + 1) * (2 * R + 1); ++i) cf.c[i] = c[i];
-    if (edge) an5d_sweep2d<T, R, BT, V, BOX, true><<<(unsigned)blocks, 32 * kWarps2D, 0, st>>>(a, cf);
-    else an5d_sweep2d<T, R, BT, V, BOX, false><<<(unsigned)blocks, 32 * kWarps2D, 0, st>>>(a, cf);
+    constexpr size_t smem = smem_bytes_2d<T, R, BT, V>();
+    auto fn = &an5d_sweep2d<T, R, BT, V, BOX>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fn<<<(unsigned)blocks, 32, smem, st>>>(a, cf);
     return cudaGetLastError();
 }
 
@@ -54,12 +56,12 @@ Instance make_instance2d() {
     i.rad = R; i.bT = BT; i.vec = V;
     i.launch2d = &launch2d<T, R, BT, V, BOX>;
     i.launch3d = nullptr;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, false>);
-    i.fn_edge = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, true>);
-    i.threads = 32 * kWarps2D;
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX>);
+    i.fn_edge = i.fn_interior;
+    i.threads = 32;
     i.tile_x_loaded = 32 * V;
     i.tile_y = 0;
-    i.smem_bytes = 0;
+    i.smem_bytes = smem_bytes_2d<T, R, BT, V>();
     return i;
 }
 
