@@ -207,35 +207,41 @@ struct DevInfo {
     double hbm_gbs = 6549.0;   // MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)
 };
 
+// Device properties and per-instance occupancy are queried once per device and cached: the
+// runtime queries are not free (measured: a per-launch query made host-side launch gaps of
+// tens of ms), and a sweep of T = 1000 steps issues hundreds of launches.
 DevInfo dev_info() {
-    DevInfo di;
+    static int cached_dev = -1;
+    static DevInfo cached;
     int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) {
-        int v = 0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) di.n_sm = v;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev) == cudaSuccess && v > 0) di.clock_ghz = v * 1e-6;
-    }
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return DevInfo{}; }
+    if (dev == cached_dev) return cached;
+    DevInfo di;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) di.n_sm = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev) == cudaSuccess && v > 0) di.clock_ghz = v * 1e-6;
+    cudaGetLastError();
     if (const char* e = getenv("AN5D_HBM_GBS")) di.hbm_gbs = atof(e);
+    cached = di;
+    cached_dev = dev;
     return di;
 }
 
 int resident_blocks(const Instance& inst) {
+    static std::vector<std::pair<const void*, int>> cache;   // (kernel, blocks/SM); one device per process
+    for (const auto& c : cache)
+        if (c.first == inst.fn_interior) return c.second;
     int nblk = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, inst.fn_interior, inst.threads,
-                                                      inst.smem_bytes) != cudaSuccess || nblk < 1) {
+    if (inst.smem_bytes > 48 * 1024)
+        cudaFuncSetAttribute(inst.fn_interior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inst.smem_bytes);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, inst.fn_interior, inst.threads, inst.smem_bytes) !=
+            cudaSuccess ||
+        nblk < 1) {
         cudaGetLastError();
-        if (inst.smem_bytes > 48 * 1024) {
-            cudaFuncSetAttribute(inst.fn_interior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inst.smem_bytes);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, inst.fn_interior, inst.threads,
-                                                              inst.smem_bytes) != cudaSuccess) {
-                cudaGetLastError();
-                nblk = 1;
-            }
-        } else {
-            nblk = 1;
-        }
+        nblk = 1;
     }
-    return std::max(1, nblk);
+    cache.emplace_back(inst.fn_interior, nblk);
+    return nblk;
 }
 
 int taps_of(const Plan& p) {
@@ -244,12 +250,18 @@ int taps_of(const Plan& p) {
     return p.ndim == 2 ? 4 * p.rad + 1 : 6 * p.rad + 1;
 }
 
-// Planner model: predicted seconds per cell-step of a configuration.
-//   HBM term: bytes moved per sweep (tile windows incl. halo and stream overlap read, compute
-//   region written) / measured HBM bandwidth;
-//   issue term: warp-instructions per sweep (taps FFMA/DFMA + shuffle/shared-memory exchange + a
-//   fixed per-level overhead) / (4 schedulers x n_SM x clock), with FP64 at half rate;
-//   waves: units / (resident units per SM x n_SM), rounded up (the paper's eff_SM).
+// Planner model: predicted seconds per cell-step of a configuration, in the
+// spirit of the paper's section 5 model (one time per resource, the max of them, a
+// waves efficiency) re-derived for this build's kernels on B200:
+//   HBM term   bytes per sweep = loaded tile windows incl. halo and stream-block overlap (read) +
+//              interior (written), / (measured copy bandwidth x eta_hbm);
+//   FMA term   FMA-pipe operations per sweep = taps x every cell the kernel computes (the whole
+//              loaded window at every level over h + 2 b_T rad (+ period) rows) /
+//              (n_SM x FMA lanes x clock x eta_fma); FP64 has half the lanes;
+//   tail       units are handed out dynamically, so the tail is about one unit: the time is
+//              multiplied by (1 + resident / n_units)  (replaces eff_SM's wave quantisation).
+// eta_* are the fractions of the measured peaks the kernels reach in steady state (tools/ runs
+// on B200: star2d1r fp32 interior loop ~0.45 of the FMA peak; streaming at ~0.75 of copy BW).
 double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, int64_t h, const DevInfo& di,
                   SweepGeom* out_geom) {
     SweepGeom g{};
@@ -257,35 +269,18 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     const int R = p.rad;
     int64_t interior = 1;
     for (int i = 0; i < p.ndim; ++i) interior *= dm.E[i] - 2 * R;
-    const int64_t steps_per_unit = g.h + 2LL * bT * R;
+    const int64_t rows_per_unit = g.h + 2LL * bT * R;
     int64_t cells_per_plane = 1;
     for (int i = 0; i < p.ndim - 1; ++i) cells_per_plane *= g.loaded[i];
-    const double bytes = (double)p.elem * ((double)g.n_units * steps_per_unit * cells_per_plane + (double)interior);
-    const double t_hbm = bytes / (di.hbm_gbs * 1e9);
-    // issue model per plane per level, in warp-instructions per thread-cell
-    const int taps = taps_of(p);
-    double fp = taps;
-    double xch;
-    const int cells_per_thread = p.ndim == 2 ? inst.vec : inst.vec * 4;
-    if (p.ndim == 2) {
-        xch = (2.0 * R + 2.0) / cells_per_thread;  // shuffles + misc per lane-level
-    } else {
-        const int vy = inst.vec;
-        const double halo_words = (p.shape == AN5D_BOX) ? ((vy + 2.0 * R) * (4 + 2.0 * R) - vy * 4)
-                                                        : (2.0 * R * vy + 2.0 * R * 4);
-        xch = (halo_words + vy + 6.0) / cells_per_thread;
-    }
-    const double fp_rate = p.dtype == AN5D_F64 ? 2.0 : 1.0;  // DFMA occupies the pipe 2 cycles
-    const double instr_per_cell_level = std::max(fp * fp_rate, fp + xch) + 0.0;
-    const double thread_cells = (double)g.n_units * steps_per_unit * cells_per_plane * bT;
-    const double warp_instr = thread_cells * instr_per_cell_level / 32.0;
-    const double t_issue = warp_instr / (4.0 * di.n_sm * di.clock_ghz * 1e9);
-    // waves
-    const int per_sm = resident_blocks(inst) * 1;
-    const double conc = (double)per_sm * di.n_sm;
-    const double waves = (double)g.n_units / conc;
-    const double eff = waves / std::ceil(waves);
-    const double t = std::max(t_hbm, t_issue) / std::max(0.05, eff);
+    const double eta_hbm = 0.75, eta_fma = p.ndim == 2 ? 0.45 : 0.35;
+    const double bytes = (double)p.elem * ((double)g.n_units * rows_per_unit * cells_per_plane + (double)interior);
+    const double t_hbm = bytes / (di.hbm_gbs * 1e9 * eta_hbm);
+    const double fma_ops = (double)g.n_units * (rows_per_unit + 2 * R + 1) * cells_per_plane * bT * taps_of(p);
+    const double lanes = p.dtype == AN5D_F64 ? 64.0 : 128.0;
+    const double t_fma = fma_ops / (di.n_sm * lanes * di.clock_ghz * 1e9 * eta_fma);
+    const double resident = (double)resident_blocks(inst) * di.n_sm;
+    const double tail = 1.0 + resident / std::max<double>(1.0, (double)g.n_units);
+    const double t = std::max(t_hbm, t_fma) * tail;
     if (out_geom) *out_geom = g;
     return t / ((double)interior * bT);
 }
@@ -315,10 +310,12 @@ an5d_status choose_config(const Plan& p, const Dims& dm, int64_t T, const an5d_c
             for (int i = 0; i < p.ndim - 1; ++i) nt *= g.ntiles[i];
             const int per_sm = resident_blocks(inst) * 1;
             const int64_t conc = (int64_t)per_sm * di.n_sm;
-            for (int w = 1; w <= 8; ++w) {
+            // stream-block lengths giving 1..32 units per resident block, and a few fixed lengths
+            for (int w : {1, 2, 4, 8, 16, 32}) {
                 const int64_t nsb = std::max<int64_t>(1, (w * conc) / std::max<int64_t>(1, nt));
                 hs.push_back(std::max<int64_t>(1, cdiv(Iout, nsb)));
             }
+            for (int64_t hh : {64, 128, 256, 512}) hs.push_back(std::min<int64_t>(hh, Iout));
             hs.push_back(Iout);
         }
         for (int64_t h : hs) {

@@ -39,12 +39,19 @@ struct Registrar {
 template <typename T, int R, int BT, int V, bool BOX>
 cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, bool /*edge*/,
                      cudaStream_t st) {
-    Coeffs<T, (2 * R + 1) * (2 * R + 1)> cf;
+    Coeffs2D<T, R> cf;
     const T* c = static_cast<const T*>(coeffs);
-    for (int i = 0; i < (2 * R + 1) * (2 * R + 1); ++i) cf.c[i] = c[i];
+    for (int i = 0; i < (2 * R + 1) * (2 * R + 1); ++i) {
+        if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
+        else cf.c[i] = c[i];
+    }
     constexpr size_t smem = smem_bytes_2d<T, R, BT, V>();
     auto fn = &an5d_sweep2d<T, R, BT, V, BOX>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
+    if (smem > 48 * 1024 && !attr_set) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
     fn<<<(unsigned)blocks, 32, smem, st>>>(a, cf);
     return cudaGetLastError();
 }
@@ -72,15 +79,16 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, int64_t blocks, b
     Coeffs<T, (2 * R + 1) * (2 * R + 1) * (2 * R + 1)> cf;
     const T* c = static_cast<const T*>(coeffs);
     for (int i = 0; i < (2 * R + 1) * (2 * R + 1) * (2 * R + 1); ++i) cf.c[i] = c[i];
-    if (edge) {
-        auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, true>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
-        fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
-    } else {
-        auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, false>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
-        fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
+    static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
+    if (!attr_set) {
+        cudaFuncSetAttribute(&an5d_sweep3d<T, R, BT, VY, BOX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)K::kSmemBytes);
+        cudaFuncSetAttribute(&an5d_sweep3d<T, R, BT, VY, BOX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)K::kSmemBytes);
+        attr_set = true;
     }
+    if (edge) an5d_sweep3d<T, R, BT, VY, BOX, true><<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
+    else an5d_sweep3d<T, R, BT, VY, BOX, false><<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
     return cudaGetLastError();
 }
 
