@@ -106,6 +106,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def _traffic(workload, cfg):
+    """DRAM bytes per launch of the dominant kernel (dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed ncu --set full summary of the same workload and configuration
+    (profiles/traffic.json, written by tools/ncu_summary.py runs), else None."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f).get(workload)
+    if not d or any(d.get(k) != cfg.get(k) for k in ("bT", "vec", "h")):
+        return None
+    return d.get("traffic_bytes")
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -141,9 +155,10 @@ def cpu_oracle_rate(name, dtype_name, n, host_grid, budget_s=12.0, max_T=None):
     g = np.ascontiguousarray(host_grid, dtype=npdt)
     cells = float(n) ** ndim
     nt = oracle.max_threads()
+    oracle.run(g, rad, shape, tab, div, 1, npdt, nthreads=nt)           # warm (page-in, threads)
     t0 = time.perf_counter()
-    oracle.run(g, rad, shape, tab, div, 1, npdt, nthreads=nt)
-    t1 = time.perf_counter() - t0
+    oracle.run(g, rad, shape, tab, div, 2, npdt, nthreads=nt)
+    t1 = (time.perf_counter() - t0) / 2                                  # seconds per time step
     T_cpu = max(1, int(budget_s / max(t1, 1e-6)))
     if max_T:
         T_cpu = min(T_cpu, max_T)
@@ -344,7 +359,7 @@ def run_an5d(args):
         achieved = alg_flops / (sweep_avg * 1e-3) / 1e12
         rl = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(fp_peak / 1e12, 2), "unit": "TFLOP/s",
               "frac": round(achieved * 1e12 / fp_peak, 4)}
-    rl["traffic"] = None
+    rl["traffic"] = _traffic(args.workload, cfg)
     rl["kernel"] = f"an5d_sweep{ndim}d<{dtype_name},R={rad},bT={cfg['bT']},vec={cfg['vec']}> (interior+edge)"
     rl["sweep_ms"] = round(sweep_avg, 4)
     rl["alg_bytes_per_launch"] = alg_bytes

@@ -461,33 +461,17 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         }
         return AN5D_OK;
     } else {
+        // one block per (tile, stream block) unit; edge units are numbered first
         Sweep3DArgs a{};
         a.src = src; a.dst = dst; a.pz = dm.pitch[0]; a.py = dm.pitch[1];
         a.Ez = dm.E[0]; a.g_off = g_off; a.gEz = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
-        a.h = g.h; a.n_sb = g.n_sb; a.sb_lo = g.sb_lo; a.sb_hi = g.sb_hi; a.wc = wc;
+        a.h = g.h; a.n_sb = g.n_sb; a.n_units = g.n_units; a.wc = wc;
         a.Ey = (int)dm.E[1]; a.Ex = (int)dm.E[2];
         a.Cy = g.C[0]; a.Cx = g.C[1]; a.Hy = g.halo[0]; a.Hx = g.halo[1];
         a.nty = (int)g.ntiles[0]; a.ntx = (int)g.ntiles[1];
-        a.ty_lo = (int)g.t_lo[0]; a.ty_hi = (int)g.t_hi[0]; a.tx_lo = (int)g.t_lo[1]; a.tx_hi = (int)g.t_hi[1];
-        if (n_edge > 0) {
-            if ((e = cudaEventRecord(p.ev_fork, st)) != cudaSuccess) return cuda_fail(e, "event record");
-            if ((e = cudaStreamWaitEvent(p.side, p.ev_fork, 0)) != cudaSuccess) return cuda_fail(e, "wait");
-            Sweep3DArgs ae = a;
-            ae.n_units = n_edge;
-            if ((e = inst->launch3d(ae, p.coeffs_dev_t.data(), n_edge, true, p.side)) != cudaSuccess)
-                return cuda_fail(e, "edge sweep launch");
-            p.launches++;
-            if ((e = cudaEventRecord(p.ev_join, p.side)) != cudaSuccess) return cuda_fail(e, "event record");
-        }
-        if (g.n_interior > 0) {
-            a.n_units = g.n_interior;
-            if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), g.n_interior, false, st)) != cudaSuccess)
-                return cuda_fail(e, "interior sweep launch");
-            p.launches++;
-        }
-    }
-    if (n_edge > 0) {
-        if ((e = cudaStreamWaitEvent(st, p.ev_join, 0)) != cudaSuccess) return cuda_fail(e, "join");
+        if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), g.n_units, false, st)) != cudaSuccess)
+            return cuda_fail(e, "sweep launch");
+        p.launches++;
     }
     return AN5D_OK;
 }

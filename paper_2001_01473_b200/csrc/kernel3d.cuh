@@ -1,32 +1,36 @@
 // kernel3d.cuh -- N.5D (2.5D spatial + b_T temporal) blocked 3D stencil sweep for sm_100a.
 //
 // PAPER.md mapping (AN5D, arXiv 2001.01473):
-//   * a thread block owns a (y, x) tile of b_Sy x b_Sx cells and streams along z, the outermost
-//     dimension (2.5D blocking);
+//   * a thread block owns a (y, x) tile and streams along z, the outermost dimension (2.5D
+//     blocking);
 //   * b_T computational streams; level T works on plane s - T*rad (fig:tier);
 //   * overlapped tiles with b_T*rad halos recomputed redundantly, compute region stored
 //     (P:166-172);
-//   * in-plane neighbours are exchanged through a DOUBLE-BUFFERED shared-memory plane, one block
-//     barrier per level (Table 1 "2 x n_thr x n_word");
 //   * stream-dimension neighbours never touch shared memory: every arriving plane of level T-1
 //     updates the 2*rad+1 in-flight output planes of level T held in registers (associative partial
 //     sums; for star the off-centre planes add one tap);
-//   * fixed register slots indexed by plane mod (2*rad+1), loop unrolled by that period;
-//     for box stencils with rad >= 2 (>= 125 taps per cell) the code size of that unroll is not
-//     worth it: the slots are rotated instead (2*rad moves per cell against (2rad+1)^3 FMAs);
-//   * the boundary ring is never computed: ring planes / cells are re-read from the sweep input
-//     whenever a level needs them.
+//   * fixed register slots indexed by plane mod (2*rad+1), stream loop unrolled by that period
+//     (P:384-389);
+//   * in-plane neighbours of other threads go through a DOUBLE-BUFFERED shared-memory exchange with
+//     one block barrier per level -- but only the rad rows a neighbour needs, not the
+//     whole sub-plane;
+//   * the boundary ring is never computed: ring planes / rows / cells that are the input of a level
+//     take their original values, read back from the on-chip plane stage.
 //
 // B200 design:
-//   * 256 threads, 16 x 16; each thread owns a VY x 4 patch of cells (register tiling: 4 x-cells =
-//     one 16-byte vector for fp32, two for fp64), so a plane of the tile is 64 x (16*VY) cells;
-//   * the streamed level-0 plane is staged by cp.async (LDGSTS, 16 bytes per request) into a ring
-//     of D shared-memory planes, D-1 planes ahead of the computation: no registers are spent on
-//     prefetch and HBM latency is covered by the pipeline depth, not by occupancy;
-//   * level 1 reads its own patch + halo straight from the staged plane (no extra store);
-//     levels >= 2 store their patch into the double-buffered exchange plane.
+//   * 256 threads = 16 (x) x 16 (y); thread (tx, ty) owns a VY x 4 patch (a 16-byte vector per row
+//     for fp32, two for fp64); a tile plane is 64 x 16 VY cells;
+//   * x neighbours: own registers + shuffles inside each 16-lane half-warp (2 rad per row); y
+//     neighbours: own registers + rad rows from the threads above / below through shared memory;
+//   * fp32 arithmetic in packed pairs (FFMA2/FMUL2) for every tap with an even x offset, scalar
+//     FFMA for odd x offsets (see lane.cuh);
+//   * level-0 planes staged by cp.async into a ring of D planes (prefetch distance PF, plus the
+//     (b_T-1)*rad planes ring pinning reads back);
+//   * one block per (tile, stream block) unit; edge units (touching the ring or the array end)
+//     are numbered first and run a separately instantiated EDGE copy of the stream loop.
 #pragma once
 #include "common.cuh"
+#include "lane.cuh"
 
 namespace an5d {
 
@@ -38,165 +42,187 @@ struct Sweep3DArgs {
     int64_t g_off, gEz;      // global index of local plane 0, global z extent (slab mode)
     int64_t out_lo, out_hi;  // local output planes [out_lo, out_hi)
     int64_t h;               // stream-block length
-    int64_t n_units;         // units handled by this launch
-    int64_t n_sb, sb_lo, sb_hi;
+    int64_t n_units;         // units of this sweep (= blocks)
+    int64_t n_sb;            // stream blocks
     int32_t* wc;             // debug store counts (dense Ez x Ey x Ex) or nullptr
     int Ey, Ex;
     int Cy, Cx;              // compute region per tile
     int Hy, Hx;              // loaded halo per side (Hy = degree*rad; Hx rounded to 16 bytes)
     int nty, ntx;            // tiles along y, x
-    int ty_lo, ty_hi, tx_lo, tx_hi;  // interior box in tile space
 };
 
-template <typename T, int R, int VY>
+constexpr int kPrefetch3D = 3;
+
+template <typename T, int R, int BT, int VY>
 struct Kernel3DTraits {
-    static constexpr int A = VecOf<T>::A;
     static constexpr int VX = 4;
     static constexpr int TXT = 16, TYT = 16;
     static constexpr int kThreads = TXT * TYT;
-    static constexpr int kTX = TXT * VX, kTY = TYT * VY;
-    static constexpr int XP = 4;                  // x padding of the smem planes (>= rad, 16B)
-    static constexpr int TXP = kTX + 2 * XP;
-    static constexpr int TYP = kTY + 2 * R;
-    static constexpr int PLANE = TYP * TXP;       // elements per smem plane
-    static constexpr int D = 3;                   // staged level-0 planes (prefetch depth D-1)
-    static constexpr size_t kSmemBytes = (size_t)(D + 2) * PLANE * sizeof(T);
+    static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // tile plane (loaded), x by y
+    static constexpr int PROWS = kTY + 2 * R;               // staged rows (R garbage pad rows per side)
+    static constexpr int PLANE = PROWS * kTX;               // elements per staged plane
+    static constexpr int D = kPrefetch3D + (BT - 1) * R + 1;  // staged planes
+    static constexpr int XROW = kTX;                        // exchange row (cells)
+    // y-halo exchange: a thread publishes the rad rows its neighbours need (top and bottom rad rows
+    // of its patch) -- possible while rad <= VY; otherwise (rad > VY) it publishes its whole patch
+    // into a padded plane and reads rad rows spanning several threads above / below
+    static constexpr bool XPLANE = R > VY;
+    static constexpr int XBAND = 2 * R * XROW;              // exchange rows of one thread row
+    static constexpr int XBUF = XPLANE ? PROWS * kTX : (TYT + 2) * XBAND;  // one exchange buffer
+    static constexpr size_t kSmemBytes = ((size_t)D * PLANE + 2 * (size_t)XBUF) * sizeof(T);
 };
 
-// Complement of the rectangle [r_lo, r_hi) x [c_lo, c_hi) in an nrows x ncols grid.
-__device__ __forceinline__ void frame2d(int64_t u, int nrows, int ncols, int r_lo, int r_hi, int c_lo,
-                                        int c_hi, int& row, int& col) {
-    const int64_t n_bot = (int64_t)r_lo * ncols;
-    if (u < n_bot) { row = (int)(u / ncols); col = (int)(u % ncols); return; }
-    u -= n_bot;
-    const int64_t n_top = (int64_t)(nrows - r_hi) * ncols;
-    if (u < n_top) { row = r_hi + (int)(u / ncols); col = (int)(u % ncols); return; }
-    u -= n_top;
-    const int w = c_lo + (ncols - c_hi);
-    row = r_lo + (int)(u / w);
-    const int i = (int)(u % w);
-    col = i < c_lo ? i : c_hi + (i - c_lo);
+// unit -> (tile y, tile x, stream block): frame tiles (those that can touch the ring or the array
+// end: first and last two in each direction) of every stream block first, then the interior
+// tiles in stream-block order 0, n_sb-1, 1, 2, ...
+__device__ __forceinline__ void unit_to_tile3d(const Sweep3DArgs& a, int64_t u, int& ty, int& tx, int64_t& sb) {
+    const int ny = a.nty, nx = a.ntx;
+    if (ny < 4 || nx < 4) {
+        const int64_t NT = (int64_t)ny * nx;
+        sb = u / NT;
+        const int t = (int)(u % NT);
+        ty = t / nx;
+        tx = t % nx;
+        return;
+    }
+    const int F = 3 * nx + (ny - 3) * 3;   // frame tiles
+    if (u < (int64_t)F * a.n_sb) {
+        sb = u / F;
+        int f = (int)(u % F);
+        if (f < 3 * nx) {
+            const int r = f / nx;
+            ty = r == 0 ? 0 : ny - r;
+            tx = f % nx;
+        } else {
+            f -= 3 * nx;
+            ty = 1 + f / 3;
+            const int c = f % 3;
+            tx = c == 0 ? 0 : nx - c;
+        }
+        return;
+    }
+    const int64_t v = u - (int64_t)F * a.n_sb;
+    const int64_t ni = (int64_t)(ny - 3) * (nx - 3);
+    const int64_t sbi = v / ni;
+    const int t = (int)(v % ni);
+    sb = sbi == 0 ? 0 : (sbi == 1 ? a.n_sb - 1 : sbi - 1);
+    ty = 1 + t / (nx - 3);
+    tx = 1 + t % (nx - 3);
 }
 
-template <bool EDGE>
-__device__ __forceinline__ void unit_to_tile3d(const Sweep3DArgs& a, int64_t u, int& ty, int& tx,
-                                               int64_t& sb) {
-    if constexpr (!EDGE) {
-        const int nix = a.tx_hi - a.tx_lo, niy = a.ty_hi - a.ty_lo;
-        tx = a.tx_lo + (int)(u % nix);
-        ty = a.ty_lo + (int)((u / nix) % niy);
-        sb = a.sb_lo + u / ((int64_t)nix * niy);
-    } else {
-        const int64_t NT = (int64_t)a.nty * a.ntx;
-        const int64_t n_bot = a.sb_lo * NT;
-        if (u < n_bot) { sb = u / NT; const int t = (int)(u % NT); ty = t / a.ntx; tx = t % a.ntx; return; }
-        u -= n_bot;
-        const int64_t n_top = (a.n_sb - a.sb_hi) * NT;
-        if (u < n_top) {
-            sb = a.sb_hi + u / NT; const int t = (int)(u % NT); ty = t / a.ntx; tx = t % a.ntx; return;
-        }
-        u -= n_top;
-        const int64_t F = NT - (int64_t)(a.ty_hi - a.ty_lo) * (a.tx_hi - a.tx_lo);
-        sb = a.sb_lo + u / F;
-        frame2d(u % F, a.nty, a.ntx, a.ty_lo, a.ty_hi, a.tx_lo, a.tx_hi, ty, tx);
-    }
-}
+struct Unit3D {
+    int cy0, cy1, cx0, cx1;      // compute region
+    int wy0, wx0;                // loaded window origin
+    int64_t p0, p1;              // output planes
+    int64_t s_first, s_end, s_a, s_b;
+    bool ring_xy;                // window touches the y/x ring or array end
+};
+
+template <typename T, int R>
+using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * (2 * R + 1)>;
 
 template <typename T, int R, int BT, int VY, bool BOX, bool EDGE>
-__global__ void __launch_bounds__(256, 1)
-an5d_sweep3d(const Sweep3DArgs a, const Coeffs<T, (2 * R + 1) * (2 * R + 1) * (2 * R + 1)> cf) {
-    using K = Kernel3DTraits<T, R, VY>;
-    constexpr int A = K::A, VX = K::VX, TXP = K::TXP, XP = K::XP, D = K::D;
+__device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
+                                             const Unit3D& g) {
+    using K = Kernel3DTraits<T, R, BT, VY>;
+    using LN = Lane<T, K::VX>;
+    using E = typename LN::E;
+    constexpr int NE = LN::NE;              // elements per patch row
+    constexpr int VX = K::VX, A = VecOf<T>::A, NCH = VX / A;
     constexpr int P = 2 * R + 1, W = 2 * R + 1;
-    constexpr int NCH = VX / A;
-    constexpr bool ROT = BOX && R >= 2;           // rotate slots instead of unrolling by P
-    constexpr int U = ROT ? 1 : P;                // unroll factor of the stream loop
-    static_assert(R <= XP, "x padding must cover the radius");
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* const smem = reinterpret_cast<T*>(smem_raw);
-
-    const int64_t unit = blockIdx.x;
-    if (unit >= a.n_units) return;
-    int tile_y, tile_x;
-    int64_t sb;
-    unit_to_tile3d<EDGE>(a, unit, tile_y, tile_x, sb);
+    constexpr int D = K::D, PF = kPrefetch3D;
+    // High-order box stencils ((2 rad+1)^3 >= 125 taps per cell): unrolling the stream loop by the
+    // slot period P would multiply an already huge loop body by P (compile time, I-cache), so the
+    // slots are rotated instead: 2*rad moves per cell and step against >= 125 FMAs.
+    constexpr bool ROT = BOX && R >= 2;
+    constexpr int U = ROT ? 1 : P;          // unroll factor of the stream loop
+    constexpr int kTX = K::kTX;
 
     const T* __restrict__ src = static_cast<const T*>(a.src);
     T* __restrict__ dst = static_cast<T*>(a.dst);
-
     const int tid = threadIdx.x;
     const int txi = tid % K::TXT, tyi = tid / K::TXT;
-    const int xs = txi * VX, ys = tyi * VY;                 // patch origin in the tile window
+    const int xs = txi * VX, ys = tyi * VY;             // patch origin in the tile window
+    const int gy0 = g.wy0 + ys, gx0 = g.wx0 + xs;       // this thread's first cell (array coords)
+    T* const stage = smem;                              // D planes of PROWS x kTX
+    T* const xch = smem + (size_t)D * K::PLANE;         // 2 exchange buffers
+    const int own = (ys + R) * kTX + xs;                // patch origin inside a staged plane
 
-    const int cy0 = R + tile_y * a.Cy, cy1 = min(cy0 + a.Cy, a.Ey - R);
-    const int cx0 = R + tile_x * a.Cx, cx1 = min(cx0 + a.Cx, a.Ex - R);
-    const int wy0 = cy0 - a.Hy, wx0 = cx0 - a.Hx;          // loaded window origin
-    const int gy0 = wy0 + ys, gx0 = wx0 + xs;               // this thread's first cell
-    const int64_t p0 = a.out_lo + sb * a.h;
-    const int64_t p1 = min(p0 + a.h, a.out_hi);
-    const int64_t s_first = p0 - (int64_t)BT * R;
-    const int64_t s_end = p1 + (int64_t)BT * R;
-
-    // smem plane element offset of this thread's patch origin
-    const int own = (ys + R) * TXP + (xs + XP);
-    T* const stage = smem;                                   // D staged level-0 planes
-    T* const xbuf = smem + D * K::PLANE;                     // 2 exchange planes
-
-    // per-thread masks (EDGE only): ring cells and store coverage
-    uint32_t ring_mask = 0;
-    if constexpr (EDGE) {
+    // per-thread masks (EDGE): loadable vectors, ring cells, store coverage
+    unsigned ld_ok = 0, ring_mask = 0, st_full = 0, st_elem = 0;
 #pragma unroll
-        for (int yy = 0; yy < VY; ++yy)
+    for (int yy = 0; yy < VY; ++yy) {
+        const int y = gy0 + yy;
+        const bool yin = y >= 0 && y < a.Ey;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+            const int x = gx0 + j * A;
+            if (!EDGE || (yin && x >= 0 && x + A <= a.Ex)) ld_ok |= 1u << (yy * NCH + j);
+            if (y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x + A <= g.cx1) st_full |= 1u << (yy * NCH + j);
+        }
+        if constexpr (EDGE) {
 #pragma unroll
             for (int xx = 0; xx < VX; ++xx) {
-                const int y = gy0 + yy, x = gx0 + xx;
-                const bool in = y >= 0 && y < a.Ey && x >= 0 && x < a.Ex;
+                const int x = gx0 + xx;
+                const bool in = yin && x >= 0 && x < a.Ex;
                 const bool ring = y < R || y >= a.Ey - R || x < R || x >= a.Ex - R;
                 if (in && ring) ring_mask |= 1u << (yy * VX + xx);
+                if (!((st_full >> (yy * NCH + xx / A)) & 1u) && y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x < g.cx1)
+                    st_elem |= 1u << (yy * VX + xx);
             }
+        }
     }
 
-    // ---- level-0 staging: cp.async of this thread's patch rows of plane q into stage slot -----
-    auto stage_plane = [&](int64_t q, T* slot) {
-        if constexpr (!EDGE) {
-            if (q < s_end) {
-                const T* gp = src + q * a.pz + (int64_t)gy0 * a.py + gx0;
+    // ---- level-0 staging ------------------------------------------------------------------------
+    auto issue_plane = [&](int64_t q, int slot) {
+        T* sl = stage + (size_t)slot * K::PLANE + own;
+        if (!EDGE || (q >= g.s_a && q < g.s_b)) {
+            const T* gp = src + q * a.pz + (int64_t)gy0 * a.py + gx0;
 #pragma unroll
-                for (int yy = 0; yy < VY; ++yy)
+            for (int yy = 0; yy < VY; ++yy)
 #pragma unroll
-                    for (int j = 0; j < NCH; ++j)
-                        cp_async16(slot + own + yy * TXP + j * A, gp + yy * a.py + j * A, 16);
-            }
-        } else {
-            if (q >= 0 && q < a.Ez && q < s_end) {
-                const T* gp = src + q * a.pz;
+                for (int j = 0; j < NCH; ++j) {
+                    if constexpr (!EDGE) {
+                        cp_async16(sl + yy * kTX + j * A, gp + yy * a.py + j * A, 16);
+                    } else {
+                        const bool full = (ld_ok >> (yy * NCH + j)) & 1u;
+                        cp_async16_pred(sl + yy * kTX + j * A, full ? gp + yy * a.py + j * A : src + R, 16, full);
+                        const int y = gy0 + yy;
+                        const bool yin = y >= 0 && y < a.Ey;
 #pragma unroll
-                for (int yy = 0; yy < VY; ++yy) {
-                    const int y = gy0 + yy;
-#pragma unroll
-                    for (int j = 0; j < NCH; ++j) {
-                        const int x = gx0 + j * A;
-                        T* sd = slot + own + yy * TXP + j * A;
-                        if (y < 0 || y >= a.Ey || x >= a.Ex || x + A <= 0) {
-                            cp_async16(sd, src, 0);                       // zero fill
-                        } else if (x >= 0) {
-                            const int nb = min(A, a.Ex - x) * (int)sizeof(T);
-                            cp_async16(sd, gp + (int64_t)y * a.py + x, nb);
-                        } else {                                          // straddles x = 0
-#pragma unroll
-                            for (int e = 0; e < A; ++e)
-                                sd[e] = (x + e >= 0) ? gp[(int64_t)y * a.py + x + e] : T(0);
+                        for (int e = 0; e < A; ++e) {
+                            const int x = gx0 + j * A + e;
+                            const bool in = yin && x >= 0 && x < a.Ex;
+                            cp_async_elem_pred<sizeof(T)>(sl + yy * kTX + j * A + e,
+                                                          in ? gp + yy * a.py + j * A + e : src + R,
+                                                          in ? (int)sizeof(T) : 0, !full);
                         }
                     }
                 }
-            }
+        } else {
+#pragma unroll
+            for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                for (int j = 0; j < NCH; ++j) cp_async16(sl + yy * kTX + j * A, src + R, 0);
         }
         cp_async_commit();
     };
+    // a patch row (VX cells) of a staged/exchange row pointer -> elements
+    auto load_row = [&](E (&P_)[NE], const T* p) {
+        T c[VX];
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) ld_vec_shared<T>(c + j * A, p + j * A);
+        LN::from_cells(P_, c);
+    };
+    auto store_row = [&](T* p, const E (&P_)[NE]) {
+        T c[VX];
+        LN::to_cells(c, P_);
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) st_vec_shared<T>(p + j * A, c + j * A);
+    };
 
-    // ---- register state --------------------------------------------------------------------------
-    T acc[BT][P][VY][VX];
+    // ---- register state ---------------------------------------------------------------------------
+    E acc[BT][P][VY][NE];
 #pragma unroll
     for (int l = 0; l < BT; ++l)
 #pragma unroll
@@ -204,188 +230,263 @@ an5d_sweep3d(const Sweep3DArgs a, const Coeffs<T, (2 * R + 1) * (2 * R + 1) * (2
 #pragma unroll
             for (int yy = 0; yy < VY; ++yy)
 #pragma unroll
-                for (int xx = 0; xx < VX; ++xx) acc[l][k][yy][xx] = T(0);
+                for (int e = 0; e < NE; ++e) acc[l][k][yy][e] = E{};
 
-    const int64_t s_a = EDGE ? max(s_first, (int64_t)0) : s_first;
-    const int64_t base0 = s_a - (s_a % U);
-    // prologue: stage planes base0 .. base0 + D - 2
+    const int64_t s_a = EDGE ? g.s_a : g.s_first;
+    const int64_t base0 = s_a - (s_a % P);
+    auto rel = [&](int64_t x) -> int { return (int)max(min(x - base0, (int64_t)(1 << 30)), -(int64_t)(1 << 30)); };
+    const int ra = rel(g.s_a), rb = rel(g.s_b);
+    const int rlo = rel((int64_t)R - a.g_off), rhi = rel(a.gEz - R - a.g_off);
+    const int rp0 = rel(g.p0), rp1 = rel(g.p1);
+    const int r_end = rel(g.s_end);
+
 #pragma unroll
-    for (int d = 0; d < D - 1; ++d) stage_plane(base0 + d, stage + (int)((base0 + d) % D) * K::PLANE);
+    for (int d = 0; d < PF; ++d) issue_plane(base0 + d, d);
 
-    int xb = 0;  // exchange buffer parity
-    for (int64_t base = base0; base < s_end; base += U) {
+    int i = 0;          // step counter since base0
+    int slot_i = 0;     // i mod D
+    int xb = 0;         // exchange buffer parity
+    for (int64_t base = base0; base < g.s_end; base += U) {
         static_for<0, U>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
             const int64_t s = base + k;
-            T* const cur = stage + (int)(s % D) * K::PLANE;
-            cp_async_wait<D - 2>();
-            __syncthreads();                                 // plane s visible; slot (s-1)%D free
-            stage_plane(s + D - 1, stage + (int)((s + D - 1) % D) * K::PLANE);
+            const int si = i;
+            cp_async_wait<PF - 1>();
+            __syncthreads();                                   // plane s visible to every thread
+            {
+                int ns = slot_i + PF;
+                if (ns >= D) ns -= D;
+                if (EDGE || si + PF < r_end) issue_plane(s + PF, ns);
+                else cp_async_commit();
+            }
+            const T* cur = stage + (size_t)slot_i * K::PLANE;
+            ++i;
+            if (++slot_i == D) slot_i = 0;
+            const bool step_pin = EDGE && (g.ring_xy || si - (BT - 1) * R < rlo || si - R >= rhi);
 
-            T u[VY][VX];
+            E u0[VY][NE];   // level-1 arrival (the staged plane s)
             static_for<1, BT + 1>([&](auto lc) {
                 constexpr int L = decltype(lc)::value;
-                const T* pl;
+                E (&u)[VY][NE] = [&]() -> E (&)[VY][NE] {
+                    if constexpr (L == 1) return u0;
+                    else return acc[L - 2][ROT ? 0 : pmod(k - (L - 2) * R - R, P)];
+                }();
+                // halo rows above / below the patch (y), as elements
+                E yh_lo[R][NE], yh_hi[R][NE];
                 if constexpr (L == 1) {
-                    pl = cur;
 #pragma unroll
-                    for (int yy = 0; yy < VY; ++yy)
+                    for (int yy = 0; yy < VY; ++yy) load_row(u0[yy], cur + own + yy * kTX);
 #pragma unroll
-                        for (int j = 0; j < NCH; ++j) ld_vec_shared<T>(&u[yy][j * A], pl + own + yy * TXP + j * A);
+                    for (int r = 0; r < R; ++r) {
+                        load_row(yh_lo[r], cur + own + (r - R) * kTX);
+                        load_row(yh_hi[r], cur + own + (VY + r) * kTX);
+                    }
                 } else {
                     if constexpr (EDGE) {
-                        const int64_t q = s - (int64_t)(L - 1) * R;
-                        const int64_t gq = q + a.g_off;
-                        if (q < 0 || q >= a.Ez) {
+                        const int qi = si - (L - 1) * R;
+                        if (step_pin && qi >= ra && qi < rb) {
+                            int qs = slot_i - 1 - (L - 1) * R;   // stage slot of plane q
+                            while (qs < 0) qs += D;
+                            const T* sq = stage + (size_t)qs * K::PLANE + own;
+                            if (qi < rlo || qi >= rhi) {
 #pragma unroll
-                            for (int yy = 0; yy < VY; ++yy)
+                                for (int yy = 0; yy < VY; ++yy) load_row(u[yy], sq + yy * kTX);
+                            } else if (g.ring_xy) {
 #pragma unroll
-                                for (int xx = 0; xx < VX; ++xx) u[yy][xx] = T(0);
-                        } else if (gq < R || gq >= a.gEz - R) {
-                            const T* gp = src + q * a.pz;
+                                for (int yy = 0; yy < VY; ++yy) {
+                                    E o[NE];
+                                    load_row(o, sq + yy * kTX);
 #pragma unroll
-                            for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                                for (int xx = 0; xx < VX; ++xx) {
-                                    const int y = gy0 + yy, x = gx0 + xx;
-                                    u[yy][xx] = (y >= 0 && y < a.Ey && x >= 0 && x < a.Ex)
-                                                    ? gp[(int64_t)y * a.py + x] : T(0);
+                                    for (int xx = 0; xx < VX; ++xx) {
+                                        T& uc = LN::cell(u[yy], xx);
+                                        uc = ((ring_mask >> (yy * VX + xx)) & 1u) ? LN::cell(o, xx) : uc;
+                                    }
                                 }
-                        } else if (ring_mask) {
-                            const T* gp = src + q * a.pz;
-#pragma unroll
-                            for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                                for (int xx = 0; xx < VX; ++xx)
-                                    if (ring_mask & (1u << (yy * VX + xx)))
-                                        u[yy][xx] = gp[(int64_t)(gy0 + yy) * a.py + gx0 + xx];
+                            }
                         }
                     }
-                    T* xw = xbuf + xb * K::PLANE;
+                    // publish the rad rows the threads above / below need, one barrier, read theirs
+                    T* xw = xch + (size_t)xb * K::XBUF;
                     xb ^= 1;
+                    if constexpr (!K::XPLANE) {
 #pragma unroll
-                    for (int yy = 0; yy < VY; ++yy)
+                        for (int r = 0; r < R; ++r) {
+                            store_row(xw + (tyi + 1) * K::XBAND + r * kTX + xs, u[r]);             // top rows
+                            store_row(xw + (tyi + 1) * K::XBAND + (R + r) * kTX + xs, u[VY - R + r]);  // bottom
+                        }
+                        __syncthreads();
 #pragma unroll
-                        for (int j = 0; j < NCH; ++j) st_vec_shared<T>(xw + own + yy * TXP + j * A, &u[yy][j * A]);
-                    __syncthreads();
-                    pl = xw;
-                }
-                // ---- gather the in-plane neighbourhood of the patch ------------------------------
-                T uh[VY + 2 * R][VX + 2 * R];
+                        for (int r = 0; r < R; ++r) {
+                            load_row(yh_lo[r], xw + tyi * K::XBAND + (R + r) * kTX + xs);    // above: its bottom
+                            load_row(yh_hi[r], xw + (tyi + 2) * K::XBAND + r * kTX + xs);    // below: its top
+                        }
+                    } else {
 #pragma unroll
-                for (int yy = 0; yy < VY; ++yy)
+                        for (int yy = 0; yy < VY; ++yy) store_row(xw + own + yy * kTX, u[yy]);
+                        __syncthreads();
 #pragma unroll
-                    for (int xx = 0; xx < VX; ++xx) uh[R + yy][R + xx] = u[yy][xx];
-#pragma unroll
-                for (int yy = -R; yy < VY + R; ++yy) {
-                    const bool own_row = yy >= 0 && yy < VY;
-                    if (!own_row) {
-#pragma unroll
-                        for (int j = 0; j < NCH; ++j)
-                            ld_vec_shared<T>(&uh[R + yy][R + j * A], pl + own + yy * TXP + j * A);
-                    }
-                    if (own_row || BOX) {
-#pragma unroll
-                        for (int r = 1; r <= R; ++r) {
-                            uh[R + yy][R - r] = pl[own + yy * TXP - r];
-                            uh[R + yy][R + VX - 1 + r] = pl[own + yy * TXP + VX - 1 + r];
+                        for (int r = 0; r < R; ++r) {
+                            load_row(yh_lo[r], xw + own + (r - R) * kTX);
+                            load_row(yh_hi[r], xw + own + (VY + r) * kTX);
                         }
                     }
                 }
-                // ---- contributions of the arriving plane q = s-(L-1)R to outputs p = q - dz ------
+                // x halo of a row: rad cells from the left / right thread of the 16-lane segment
+                auto xhalo = [&](const E (&row)[NE], T (&hl)[R], T (&hh)[R]) {
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        hh[m] = __shfl_down_sync(0xffffffffu, LN::cell(row, m), 1, K::TXT);
+                        hl[m] = __shfl_up_sync(0xffffffffu, LN::cell(row, VX - R + m), 1, K::TXT);
+                    }
+                };
+                // extended row accessor: row index yr in [-R, VY+R), cell c in [-R, VX+R)
+                auto rowref = [&](int yr) -> const E (&)[NE] {
+                    return yr < 0 ? yh_lo[yr + R] : (yr >= VY ? yh_hi[yr - VY] : u[yr]);
+                };
+                constexpr int XR = BOX ? VY + 2 * R : VY;       // rows needing an x halo
+                T hl[XR][R], hh[XR][R];
+#pragma unroll
+                for (int t = 0; t < XR; ++t) xhalo(rowref(BOX ? t - R : t), hl[t], hh[t]);
+                auto X = [&](int yr, int c) -> T {
+                    const int t = BOX ? yr + R : yr;
+                    return c < 0 ? hl[t][c + R] : (c >= VX ? hh[t][c - VX] : LN::cell(rowref(yr), c));
+                };
+                // contributions of arriving plane q = s - (L-1) R to output planes p = q - dz
                 static_for<0, 2 * R + 1>([&](auto dc) {
                     constexpr int dz = R - decltype(dc)::value;
-                    constexpr int slot = ROT ? (R - dz) : pmod(k - (L - 1) * R - dz, P);
+                    constexpr int slot = ROT ? R - dz : pmod(k - (L - 1) * R - dz, P);
+                    auto tap = [&](const E c, int dy, int dx, bool first) {
+#pragma unroll
+                        for (int yy = 0; yy < VY; ++yy) {
+                            if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                                for (int e = 0; e < NE; ++e) {
+                                    const T q = X(yy + dy, e + dx);
+                                    acc[L - 1][slot][yy][e] = first ? LN::mul(c, q) : LN::fma(c, q, acc[L - 1][slot][yy][e]);
+                                }
+                            } else {
+                                if ((dx & 1) == 0) {
+#pragma unroll
+                                    for (int e = 0; e < NE; ++e) {
+                                        const int j = 2 * e + dx;
+                                        const E q = (j >= 0 && j + 1 < VX) ? rowref(yy + dy)[j >> 1]
+                                                                           : make_float2(X(yy + dy, j), X(yy + dy, j + 1));
+                                        acc[L - 1][slot][yy][e] =
+                                            first ? LN::mul(c, q) : LN::fma(c, q, acc[L - 1][slot][yy][e]);
+                                    }
+                                } else {
+#pragma unroll
+                                    for (int e = 0; e < NE; ++e) {
+                                        E& o = acc[L - 1][slot][yy][e];
+                                        o.x = first ? c.x * X(yy + dy, 2 * e + dx) : fmaf(c.x, X(yy + dy, 2 * e + dx), o.x);
+                                        o.y = first ? c.x * X(yy + dy, 2 * e + 1 + dx)
+                                                    : fmaf(c.x, X(yy + dy, 2 * e + 1 + dx), o.y);
+                                    }
+                                }
+                            }
+                        }
+                    };
+                    auto C = [&](int dy, int dx) { return cf.c[((dz + R) * W + (dy + R)) * W + (dx + R)]; };
                     if constexpr (BOX) {
 #pragma unroll
                         for (int dy = -R; dy <= R; ++dy)
 #pragma unroll
-                            for (int dx = -R; dx <= R; ++dx) {
-                                const T c = cf.c[((dz + R) * W + (dy + R)) * W + (dx + R)];
-#pragma unroll
-                                for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                                    for (int xx = 0; xx < VX; ++xx) {
-                                        T& o = acc[L - 1][slot][yy][xx];
-                                        const T f = uh[R + yy + dy][R + xx + dx];
-                                        if (dz == -R && dy == -R && dx == -R) o = c * f;
-                                        else o = fma(c, f, o);
-                                    }
-                            }
+                            for (int dx = -R; dx <= R; ++dx) tap(C(dy, dx), dy, dx, dz == -R && dy == -R && dx == -R);
                     } else if constexpr (dz != 0) {
-                        const T c = cf.c[((dz + R) * W + R) * W + R];
-#pragma unroll
-                        for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                            for (int xx = 0; xx < VX; ++xx) {
-                                T& o = acc[L - 1][slot][yy][xx];
-                                if (dz == -R) o = c * u[yy][xx];
-                                else o = fma(c, u[yy][xx], o);
-                            }
+                        tap(C(0, 0), 0, 0, dz == -R);
                     } else {
                         // in-plane cross in lexicographic (dy, dx) order
 #pragma unroll
-                        for (int dy = -R; dy <= R; ++dy) {
+                        for (int dy = -R; dy < 0; ++dy) tap(C(dy, 0), dy, 0, false);
 #pragma unroll
-                            for (int dx = -R; dx <= R; ++dx) {
-                                if (dy != 0 && dx != 0) continue;
-                                const T c = cf.c[(R * W + (dy + R)) * W + (dx + R)];
+                        for (int dx = -R; dx <= R; ++dx) tap(C(0, dx), 0, dx, false);
 #pragma unroll
-                                for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                                    for (int xx = 0; xx < VX; ++xx) {
-                                        T& o = acc[L - 1][slot][yy][xx];
-                                        o = fma(c, uh[R + yy + dy][R + xx + dx], o);
-                                    }
-                            }
-                        }
+                        for (int dy = 1; dy <= R; ++dy) tap(C(dy, 0), dy, 0, false);
                     }
                 });
-                constexpr int done = ROT ? 0 : pmod(k - (L - 1) * R - R, P);
+            });
+            // ---- STORE level BT plane p = s - BT*R, compute region only ----------------------------
+            const int pi = si - BT * R;
+            if (pi >= rp0 && pi < rp1) {
+                const int64_t p = s - (int64_t)BT * R;
+                const auto& fin = acc[BT - 1][ROT ? 0 : pmod(k - (BT - 1) * R - R, P)];
+                T* op = dst + p * a.pz + (int64_t)gy0 * a.py + gx0;
 #pragma unroll
-                for (int yy = 0; yy < VY; ++yy)
+                for (int yy = 0; yy < VY; ++yy) {
+                    T c[VX];
+                    LN::to_cells(c, fin[yy]);
 #pragma unroll
-                    for (int xx = 0; xx < VX; ++xx) u[yy][xx] = acc[L - 1][done][yy][xx];
-                if constexpr (ROT) {
+                    for (int j = 0; j < NCH; ++j) {
+                        if ((st_full >> (yy * NCH + j)) & 1u) st_vec_global<T>(op + yy * a.py + j * A, c + j * A);
+                        if constexpr (EDGE) {
+#pragma unroll
+                            for (int e = 0; e < A; ++e)
+                                if ((st_elem >> (yy * VX + j * A + e)) & 1u) op[yy * a.py + j * A + e] = c[j * A + e];
+                        }
+                    }
+                    if (a.wc) {
+                        const int y = gy0 + yy;
+#pragma unroll
+                        for (int xx = 0; xx < VX; ++xx) {
+                            const int x = gx0 + xx;
+                            if (y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x < g.cx1)
+                                atomicAdd(a.wc + (p * a.Ey + y) * (int64_t)a.Ex + x, 1);
+                        }
+                    }
+                }
+            }
+            if constexpr (ROT) {
+                // slot j <- slot j+1: slot 0 (just completed and consumed) is recycled as the last
+#pragma unroll
+                for (int l = 0; l < BT; ++l)
 #pragma unroll
                     for (int j = 0; j + 1 < P; ++j)
 #pragma unroll
                         for (int yy = 0; yy < VY; ++yy)
 #pragma unroll
-                            for (int xx = 0; xx < VX; ++xx) acc[L - 1][j][yy][xx] = acc[L - 1][j + 1][yy][xx];
-                }
-            });
-            // ---- STORE level BT plane p = s - BT*R, compute region only ----------------------------
-            const int64_t p = s - (int64_t)BT * R;
-            if (p >= p0 && p < p1) {
-                T* op = dst + p * a.pz;
-#pragma unroll
-                for (int yy = 0; yy < VY; ++yy) {
-                    const int y = gy0 + yy;
-                    if (y < cy0 || y >= cy1) continue;
-#pragma unroll
-                    for (int j = 0; j < NCH; ++j) {
-                        const int x = gx0 + j * A;
-                        if (x >= cx0 && x + A <= cx1) {
-                            st_vec_global<T>(op + (int64_t)y * a.py + x, &u[yy][j * A]);
-                        } else if (EDGE && x + A > cx0 && x < cx1) {
-#pragma unroll
-                            for (int e = 0; e < A; ++e)
-                                if (x + e >= cx0 && x + e < cx1) op[(int64_t)y * a.py + x + e] = u[yy][j * A + e];
-                        }
-                    }
-                    if (a.wc) {
-#pragma unroll
-                        for (int xx = 0; xx < VX; ++xx) {
-                            const int x = gx0 + xx;
-                            if (x >= cx0 && x < cx1) atomicAdd(a.wc + (p * a.Ey + y) * (int64_t)a.Ex + x, 1);
-                        }
-                    }
-                }
+                            for (int e = 0; e < NE; ++e) acc[l][j][yy][e] = acc[l][j + 1][yy][e];
             }
         });
     }
     cp_async_wait<0>();
+}
+
+// resident blocks per SM the register budget is shaped for: small fp32 patches (VY <= 2) fit two
+// blocks (<= 128 registers/thread), so one block's barrier and latency stalls overlap the other's;
+// fp64 (twice the registers per cell) and high-order box keep one block and up to 255 registers
+template <typename T, int VY, int R, bool BOX> constexpr int min_blocks_3d() {
+    return (sizeof(T) == 4 && VY <= 2 && !(BOX && R >= 2)) ? 2 : 1;
+}
+
+template <typename T, int R, int BT, int VY, bool BOX>
+__global__ void __launch_bounds__(256, min_blocks_3d<T, VY, R, BOX>())
+an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf) {
+    using K = Kernel3DTraits<T, R, BT, VY>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* const smem = reinterpret_cast<T*>(smem_raw);
+    const int64_t unit = blockIdx.x;
+    if (unit >= a.n_units) return;
+    int ty, tx;
+    int64_t sb;
+    unit_to_tile3d(a, unit, ty, tx, sb);
+    Unit3D g;
+    g.cy0 = R + ty * a.Cy;
+    g.cy1 = min(g.cy0 + a.Cy, a.Ey - R);
+    g.cx0 = R + tx * a.Cx;
+    g.cx1 = min(g.cx0 + a.Cx, a.Ex - R);
+    g.wy0 = g.cy0 - a.Hy;
+    g.wx0 = g.cx0 - a.Hx;
+    g.p0 = a.out_lo + sb * a.h;
+    g.p1 = min(g.p0 + a.h, a.out_hi);
+    g.s_first = g.p0 - (int64_t)BT * R;
+    g.s_end = g.p1 + (int64_t)BT * R;
+    g.s_a = max(g.s_first, (int64_t)0);
+    g.s_b = min(g.s_end, a.Ez);
+    g.ring_xy = g.wy0 < R || g.wy0 + K::kTY > a.Ey - R || g.wx0 < R || g.wx0 + K::kTX > a.Ex - R;
+    const bool zedge = (g.s_first + a.g_off < R) || (g.s_end - 1 + a.g_off >= a.gEz - R) || g.s_first < 0 ||
+                       g.s_end > a.Ez;
+    if (g.ring_xy || zedge) sweep3d_unit<T, R, BT, VY, BOX, true>(a, cf, smem, g);
+    else sweep3d_unit<T, R, BT, VY, BOX, false>(a, cf, smem, g);
 }
 
 }  // namespace an5d

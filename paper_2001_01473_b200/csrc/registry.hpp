@@ -73,35 +73,36 @@ Instance make_instance2d() {
 }
 
 template <typename T, int R, int BT, int VY, bool BOX>
-cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, int64_t blocks, bool edge,
+cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, int64_t blocks, bool /*edge*/,
                      cudaStream_t st) {
-    using K = Kernel3DTraits<T, R, VY>;
-    Coeffs<T, (2 * R + 1) * (2 * R + 1) * (2 * R + 1)> cf;
+    using K = Kernel3DTraits<T, R, BT, VY>;
+    constexpr int N = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
+    Coeffs3D<T, R> cf;
     const T* c = static_cast<const T*>(coeffs);
-    for (int i = 0; i < (2 * R + 1) * (2 * R + 1) * (2 * R + 1); ++i) cf.c[i] = c[i];
+    for (int i = 0; i < N; ++i) {
+        if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
+        else cf.c[i] = c[i];
+    }
+    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (!attr_set) {
-        cudaFuncSetAttribute(&an5d_sweep3d<T, R, BT, VY, BOX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)K::kSmemBytes);
-        cudaFuncSetAttribute(&an5d_sweep3d<T, R, BT, VY, BOX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)K::kSmemBytes);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
         attr_set = true;
     }
-    if (edge) an5d_sweep3d<T, R, BT, VY, BOX, true><<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
-    else an5d_sweep3d<T, R, BT, VY, BOX, false><<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
+    fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf);
     return cudaGetLastError();
 }
 
 template <typename T, int R, int BT, int VY, bool BOX>
 Instance make_instance3d() {
-    using K = Kernel3DTraits<T, R, VY>;
+    using K = Kernel3DTraits<T, R, BT, VY>;
     Instance i{};
     i.ndim = 3; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
     i.rad = R; i.bT = BT; i.vec = VY;
     i.launch2d = nullptr;
     i.launch3d = &launch3d<T, R, BT, VY, BOX>;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, false>);
-    i.fn_edge = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, true>);
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX>);
+    i.fn_edge = i.fn_interior;
     i.threads = K::kThreads;
     i.tile_x_loaded = K::kTX;
     i.tile_y = K::kTY;

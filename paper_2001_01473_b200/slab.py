@@ -271,6 +271,10 @@ def bench_main(args, workloads):
         step(i)
     torch.cuda.synchronize()
     dist.barrier()
+    l0 = st.last_launch_count()
+    step(0)
+    torch.cuda.synchronize()
+    launches_per_step = st.last_launch_count() - l0 + 1   # + the ring copy
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         dist.barrier()
@@ -285,6 +289,34 @@ def bench_main(args, workloads):
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    # end to end: host (pinned) slab in, owned planes out, every step, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        n_in = a.untyped_storage().nbytes() // a.element_size()
+        flat_a = torch.empty(0, dtype=dtype, device=dev).set_(a.untyped_storage())
+        host_in = torch.empty(n_in, dtype=dtype, pin_memory=True)
+        host_in.copy_(flat_a.cpu())
+        owned = _plane_view(b, s.out_lo, s.out_hi - s.out_lo)
+        host_out = torch.empty(owned.numel(), dtype=dtype, pin_memory=True)
+        k_e2e = max(2, min(args.steps, 5))
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k_e2e):
+            flat_a.copy_(host_in, non_blocking=True)
+            run_distributed(st, s, (a, b), T, cfg, comm_stream=comm)
+            host_out.copy_(owned, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nb = torch.tensor([float(host_in.numel() * host_in.element_size()),
+                           float(host_out.numel() * host_out.element_size())], dtype=torch.float64, device=dev)
+        dist.all_reduce(nb)
+        e2e = {"value": round(float(n) ** ndim * T / (float(te.item()) * 1e-3) / 1e9, 3), "unit": "GCells/s",
+               "h2d_bytes_per_step": int(nb[0].item()), "d2h_bytes_per_step": int(nb[1].item()),
+               "ms_per_step": round(float(te.item()), 3), "steps": k_e2e}
     cells = float(n) ** ndim
     gcells = cells * T / (ms * 1e-3) / 1e9
     F = perf.flops_per_cell(ndim, rad, shape, div != 1.0)
@@ -298,8 +330,8 @@ def bench_main(args, workloads):
             "config": {"workload": args.workload, "stencil": name, "grid": list(gext), "T": T, "bT": cfg["bT"],
                        "vec": cfg["vec"], "h": cfg["h"], "parallelism": f"slab{ws} (outermost dim, NCCL halo)",
                        "l2": "inputs larger than L2"},
-            "gflops": round(gcells * F, 2), "roofline": None, "cpu_baseline": None, "e2e": None,
-            "gpu_launches": None,
+            "gflops": round(gcells * F, 2), "roofline": None, "cpu_baseline": None, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps * ws,
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
         }
         print(json.dumps(line), flush=True)

@@ -202,3 +202,40 @@ def test_run_split_equals_single_run(an5d):
     torch.cuda.synchronize()
     err = rel_linf(b3.cpu().numpy(), full.cpu().numpy(), rad)
     assert err <= 1e-6
+
+
+@pytest.mark.parametrize("name,n_int,T,bT,nslab", [
+    ("star2d1r", (97, 131), 9, 4, 3),
+    ("box2d2r", (61, 77), 7, 3, 2),
+    ("star3d1r", (41, 37, 70), 7, 3, 3),
+    ("j3d27pt", (33, 19, 45), 5, 2, 2),
+])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_slab_loopback_bit_identical(an5d, name, n_int, T, bT, nslab, dtype):
+    """Multi-GPU slab bookkeeping on one device (SURVEY §4 loopback mode): the streaming dim split
+    into slabs with ghost planes, an5d_sweep in slab mode, ghosts exchanged by device copies.  The
+    gathered owned planes must equal the single-domain an5d_run bit-for-bit (same per-cell
+    arithmetic) and the oracle within tolerance."""
+    from paper_2001_01473_b200 import slab
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    gext = tuple(v + 2 * rad for v in n_int)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, gext)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    cfg = st.plan_config(gext, T, {"bT": bT, "h": 8})
+    ref, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+    parts = slab.partition(gext[0], rad, nslab, cfg["bT"] * rad)
+    bufs = []
+    for s in parts:
+        loc = g[s.loc_lo:s.loc_hi]
+        a = an5d.to_grid(torch.from_numpy(loc.astype(NP[dtype])).cuda(), rad)
+        b = an5d.empty_grid(loc.shape, rad, dtype)
+        b.fill_(float("nan"))
+        bufs.append((a, b))
+    outs = slab.run_loopback(st, parts, bufs, T, cfg)
+    torch.cuda.synchronize()
+    got = np.concatenate([o.cpu().numpy()[s.out_lo:s.out_hi] for s, o in zip(parts, outs)])
+    assert np.array_equal(got, ref[rad:gext[0] - rad])
+    exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+    full = ref.copy()
+    full[rad:gext[0] - rad] = got
+    assert rel_linf(full, exp, rad) <= TOL[dtype]
