@@ -26,8 +26,9 @@
 //     FFMA for odd x offsets (see lane.cuh);
 //   * level-0 planes staged by cp.async into a ring of D planes (prefetch distance PF, plus the
 //     (b_T-1)*rad planes ring pinning reads back);
-//   * one block per (tile, stream block) unit; edge units (touching the ring or the array end)
-//     are numbered first and run a separately instantiated EDGE copy of the stream loop.
+//   * one block per (tile, stream block) unit; units whose tile window touches the x/y ring or the
+//     array end are numbered first and run a separately instantiated EDGE copy of the stream loop
+//     (the z ring / z array ends cost a uniform per-step check in both copies).
 #pragma once
 #include "common.cuh"
 #include "lane.cuh"
@@ -176,7 +177,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // ---- level-0 staging ------------------------------------------------------------------------
     auto issue_plane = [&](int64_t q, int slot) {
         T* sl = stage + (size_t)slot * K::PLANE + own;
-        if (!EDGE || (q >= g.s_a && q < g.s_b)) {
+        if (q >= g.s_a && q < g.s_b) {
             const T* gp = src + q * a.pz + (int64_t)gy0 * a.py + gx0;
 #pragma unroll
             for (int yy = 0; yy < VY; ++yy)
@@ -232,13 +233,12 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
                 for (int e = 0; e < NE; ++e) acc[l][k][yy][e] = E{};
 
-    const int64_t s_a = EDGE ? g.s_a : g.s_first;
+    const int64_t s_a = g.s_a;
     const int64_t base0 = s_a - (s_a % P);
     auto rel = [&](int64_t x) -> int { return (int)max(min(x - base0, (int64_t)(1 << 30)), -(int64_t)(1 << 30)); };
     const int ra = rel(g.s_a), rb = rel(g.s_b);
     const int rlo = rel((int64_t)R - a.g_off), rhi = rel(a.gEz - R - a.g_off);
     const int rp0 = rel(g.p0), rp1 = rel(g.p1);
-    const int r_end = rel(g.s_end);
 
 #pragma unroll
     for (int d = 0; d < PF; ++d) issue_plane(base0 + d, d);
@@ -256,13 +256,14 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             {
                 int ns = slot_i + PF;
                 if (ns >= D) ns -= D;
-                if (EDGE || si + PF < r_end) issue_plane(s + PF, ns);
-                else cp_async_commit();
+                issue_plane(s + PF, ns);   // planes outside [s_a, s_b) are zero-filled, no traffic
             }
             const T* cur = stage + (size_t)slot_i * K::PLANE;
             ++i;
             if (++slot_i == D) slot_i = 0;
-            const bool step_pin = EDGE && (g.ring_xy || si - (BT - 1) * R < rlo || si - R >= rhi);
+            // does any level's arrival need pinning this step?  z-ring planes (any unit, a few steps
+            // at the ends of the array) or x/y-ring cells (EDGE units, every step)
+            const bool step_pin = (EDGE && g.ring_xy) || si - (BT - 1) * R < rlo || si - R >= rhi;
 
             E u0[VY][NE];   // level-1 arrival (the staged plane s)
             static_for<1, BT + 1>([&](auto lc) {
@@ -282,7 +283,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                         load_row(yh_hi[r], cur + own + (VY + r) * kTX);
                     }
                 } else {
-                    if constexpr (EDGE) {
+                    {
                         const int qi = si - (L - 1) * R;
                         if (step_pin && qi >= ra && qi < rb) {
                             int qs = slot_i - 1 - (L - 1) * R;   // stage slot of plane q
@@ -291,7 +292,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                             if (qi < rlo || qi >= rhi) {
 #pragma unroll
                                 for (int yy = 0; yy < VY; ++yy) load_row(u[yy], sq + yy * kTX);
-                            } else if (g.ring_xy) {
+                            } else if (EDGE && g.ring_xy) {
 #pragma unroll
                                 for (int yy = 0; yy < VY; ++yy) {
                                     E o[NE];
@@ -483,9 +484,9 @@ an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf) {
     g.s_a = max(g.s_first, (int64_t)0);
     g.s_b = min(g.s_end, a.Ez);
     g.ring_xy = g.wy0 < R || g.wy0 + K::kTY > a.Ey - R || g.wx0 < R || g.wx0 + K::kTX > a.Ex - R;
-    const bool zedge = (g.s_first + a.g_off < R) || (g.s_end - 1 + a.g_off >= a.gEz - R) || g.s_first < 0 ||
-                       g.s_end > a.Ez;
-    if (g.ring_xy || zedge) sweep3d_unit<T, R, BT, VY, BOX, true>(a, cf, smem, g);
+    // z-ring planes and the array's z ends are handled by both variants (uniform per-step checks);
+    // the EDGE variant is only for tiles whose window touches the x/y ring or the array end
+    if (g.ring_xy) sweep3d_unit<T, R, BT, VY, BOX, true>(a, cf, smem, g);
     else sweep3d_unit<T, R, BT, VY, BOX, false>(a, cf, smem, g);
 }
 
