@@ -62,7 +62,6 @@ struct Kernel3DTraits {
     static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // tile plane (loaded), x by y
     static constexpr int PROWS = kTY + 2 * R;               // staged rows (R garbage pad rows per side)
     static constexpr int PLANE = PROWS * kTX;               // elements per staged plane
-    static constexpr int D = kPrefetch3D + (BT - 1) * R + 1;  // staged planes
     static constexpr int XROW = kTX;                        // exchange row (cells)
     // y-halo exchange: a thread publishes the rad rows its neighbours need (top and bottom rad rows
     // of its patch) -- possible while rad <= VY; otherwise (rad > VY) it publishes its whole patch
@@ -70,7 +69,23 @@ struct Kernel3DTraits {
     static constexpr bool XPLANE = R > VY;
     static constexpr int XBAND = 2 * R * XROW;              // exchange rows of one thread row
     static constexpr int XBUF = XPLANE ? PROWS * kTX : (TYT + 2) * XBAND;  // one exchange buffer
-    static constexpr size_t kSmemBytes = ((size_t)D * PLANE + 2 * (size_t)XBUF) * sizeof(T);
+    // Level skew SK (see sweep3d_unit): with SK = 1 level L at step s takes the plane level L-1
+    // completed at step s-1, so all levels' halo rows are exchanged together behind the one
+    // barrier a step has anyway (1 barrier per plane instead of b_T).  Costs deeper staging (the
+    // arrival of level L is (L-1)(rad+1) planes old) and an exchange buffer per level.  Off for
+    // rotated-slot kernels and where the shared memory would not fit.
+    static constexpr int D0 = kPrefetch3D + (BT - 1) * R + 1;                       // SK = 0
+    static constexpr int D1 = kPrefetch3D + (BT >= 2 ? (BT - 2) * (R + 1) + R : 0) + 1;  // SK = 1
+    static constexpr size_t smem_of(int d, int nxb) { return ((size_t)d * PLANE + (size_t)nxb * XBUF) * sizeof(T); }
+    static constexpr size_t kSmem1 = smem_of(D1, 2 * (BT - 1));
+#ifndef AN5D_SK3D
+    static constexpr int SK = (BT >= 2 && kSmem1 <= 220 * 1024) ? 1 : 0;
+#else
+    static constexpr int SK = AN5D_SK3D && BT >= 2 && kSmem1 <= 220 * 1024;
+#endif
+    static constexpr int D = SK ? D1 : D0;                  // staged planes
+    static constexpr int NXB = SK ? 2 * (BT - 1) : 2;       // exchange buffers
+    static constexpr size_t kSmemBytes = smem_of(D, NXB);
 };
 
 // unit -> (tile y, tile x, stream block): frame tiles (those that can touch the ring or the array
@@ -137,6 +152,12 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // slots are rotated instead: 2*rad moves per cell and step against >= 125 FMAs.
     constexpr bool ROT = BOX && R >= 2;
     constexpr int U = ROT ? 1 : P;          // unroll factor of the stream loop
+    // level skew (traits): SK = 1 -> level L at step s consumes level L-1's plane of step s-1;
+    // levels run top-down inside a step (a level reads its arrival slot before the level below
+    // recycles it); every level's halo rows travel through one exchange per step
+    constexpr int SK = (K::SK && !ROT) ? 1 : 0;
+    // (a rotated-slot kernel runs unskewed inside the skewed traits' buffers: D1 >= D0, >= 2 buffers)
+    constexpr int DL = R + SK;              // plane delay per level
     constexpr int kTX = K::kTX;
 
     const T* __restrict__ src = static_cast<const T*>(a.src);
@@ -243,10 +264,57 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
     for (int d = 0; d < PF; ++d) issue_plane(base0 + d, d);
 
+    // pin plane qi (relative index) of a patch to its original ring values, read from the stage
+    auto pin = [&](E (&u)[VY][NE], int qi) {
+        if (qi < ra || qi >= rb) return;                  // not in the array: feeds nothing kept
+        const T* sq = stage + (size_t)(qi % D) * K::PLANE + own;
+        if (qi < rlo || qi >= rhi) {                      // z-ring plane: every cell
+#pragma unroll
+            for (int yy = 0; yy < VY; ++yy) load_row(u[yy], sq + yy * kTX);
+        } else if (EDGE && g.ring_xy) {                   // x/y-ring cells of this thread
+#pragma unroll
+            for (int yy = 0; yy < VY; ++yy) {
+                E o[NE];
+                load_row(o, sq + yy * kTX);
+#pragma unroll
+                for (int xx = 0; xx < VX; ++xx) {
+                    T& uc = LN::cell(u[yy], xx);
+                    uc = ((ring_mask >> (yy * VX + xx)) & 1u) ? LN::cell(o, xx) : uc;
+                }
+            }
+        }
+    };
+    // publish the rows of patch u the threads above / below need; read theirs back
+    auto publish = [&](T* xw, const E (&u)[VY][NE]) {
+        if constexpr (!K::XPLANE) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                store_row(xw + (tyi + 1) * K::XBAND + r * kTX + xs, u[r]);                 // top rows
+                store_row(xw + (tyi + 1) * K::XBAND + (R + r) * kTX + xs, u[VY - R + r]);  // bottom rows
+            }
+        } else {
+#pragma unroll
+            for (int yy = 0; yy < VY; ++yy) store_row(xw + own + yy * kTX, u[yy]);
+        }
+    };
+    auto read_halo = [&](const T* xw, E (&lo)[R][NE], E (&hi)[R][NE]) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if constexpr (!K::XPLANE) {
+                load_row(lo[r], xw + tyi * K::XBAND + (R + r) * kTX + xs);         // above: its bottom rows
+                load_row(hi[r], xw + (tyi + 2) * K::XBAND + r * kTX + xs);         // below: its top rows
+            } else {
+                load_row(lo[r], xw + own + (r - R) * kTX);
+                load_row(hi[r], xw + own + (VY + r) * kTX);
+            }
+        }
+    };
+
     int i = 0;          // step counter since base0
     int slot_i = 0;     // i mod D
     int xb = 0;         // exchange buffer parity
-    for (int64_t base = base0; base < g.s_end; base += U) {
+    const int64_t s_stop = g.s_end + (int64_t)(BT - 1) * SK;
+    for (int64_t base = base0; base < s_stop; base += U) {
         static_for<0, U>([&](auto kc) {
             constexpr int k = decltype(kc)::value;
             const int64_t s = base + k;
@@ -262,15 +330,18 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             ++i;
             if (++slot_i == D) slot_i = 0;
             // does any level's arrival need pinning this step?  z-ring planes (any unit, a few steps
-            // at the ends of the array) or x/y-ring cells (EDGE units, every step)
-            const bool step_pin = (EDGE && g.ring_xy) || si - (BT - 1) * R < rlo || si - R >= rhi;
+            // at the ends of the array) or x/y-ring cells (EDGE units, every step).  SK = 1 pins at
+            // completion (end of step) the planes p = si - (l-1) DL - R, l < b_T.
+            const bool step_pin = (EDGE && g.ring_xy) ||
+                                  (SK ? (si - (BT - 2) * DL - R < rlo || si - R >= rhi)
+                                      : (si - (BT - 1) * R < rlo || si - R >= rhi));
 
             E u0[VY][NE];   // level-1 arrival (the staged plane s)
             static_for<1, BT + 1>([&](auto lc) {
-                constexpr int L = decltype(lc)::value;
+                constexpr int L = SK ? BT + 1 - decltype(lc)::value : decltype(lc)::value;
                 E (&u)[VY][NE] = [&]() -> E (&)[VY][NE] {
                     if constexpr (L == 1) return u0;
-                    else return acc[L - 2][ROT ? 0 : pmod(k - (L - 2) * R - R, P)];
+                    else return acc[L - 2][ROT ? 0 : pmod(k - SK - (L - 2) * DL - R, P)];
                 }();
                 // halo rows above / below the patch (y), as elements
                 E yh_lo[R][NE], yh_hi[R][NE];
@@ -282,55 +353,17 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                         load_row(yh_lo[r], cur + own + (r - R) * kTX);
                         load_row(yh_hi[r], cur + own + (VY + r) * kTX);
                     }
+                } else if constexpr (SK) {
+                    // halo rows of level L-1's plane of the previous step, exchanged at its end
+                    read_halo(xch + (size_t)(xb * (BT - 1) + (L - 2)) * K::XBUF, yh_lo, yh_hi);
                 } else {
-                    {
-                        const int qi = si - (L - 1) * R;
-                        if (step_pin && qi >= ra && qi < rb) {
-                            int qs = slot_i - 1 - (L - 1) * R;   // stage slot of plane q
-                            while (qs < 0) qs += D;
-                            const T* sq = stage + (size_t)qs * K::PLANE + own;
-                            if (qi < rlo || qi >= rhi) {
-#pragma unroll
-                                for (int yy = 0; yy < VY; ++yy) load_row(u[yy], sq + yy * kTX);
-                            } else if (EDGE && g.ring_xy) {
-#pragma unroll
-                                for (int yy = 0; yy < VY; ++yy) {
-                                    E o[NE];
-                                    load_row(o, sq + yy * kTX);
-#pragma unroll
-                                    for (int xx = 0; xx < VX; ++xx) {
-                                        T& uc = LN::cell(u[yy], xx);
-                                        uc = ((ring_mask >> (yy * VX + xx)) & 1u) ? LN::cell(o, xx) : uc;
-                                    }
-                                }
-                            }
-                        }
-                    }
+                    if (step_pin) pin(u, si - (L - 1) * R);
                     // publish the rad rows the threads above / below need, one barrier, read theirs
                     T* xw = xch + (size_t)xb * K::XBUF;
                     xb ^= 1;
-                    if constexpr (!K::XPLANE) {
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            store_row(xw + (tyi + 1) * K::XBAND + r * kTX + xs, u[r]);             // top rows
-                            store_row(xw + (tyi + 1) * K::XBAND + (R + r) * kTX + xs, u[VY - R + r]);  // bottom
-                        }
-                        __syncthreads();
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            load_row(yh_lo[r], xw + tyi * K::XBAND + (R + r) * kTX + xs);    // above: its bottom
-                            load_row(yh_hi[r], xw + (tyi + 2) * K::XBAND + r * kTX + xs);    // below: its top
-                        }
-                    } else {
-#pragma unroll
-                        for (int yy = 0; yy < VY; ++yy) store_row(xw + own + yy * kTX, u[yy]);
-                        __syncthreads();
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            load_row(yh_lo[r], xw + own + (r - R) * kTX);
-                            load_row(yh_hi[r], xw + own + (VY + r) * kTX);
-                        }
-                    }
+                    publish(xw, u);
+                    __syncthreads();
+                    read_halo(xw, yh_lo, yh_hi);
                 }
                 // x halo of a row: rad cells from the left / right thread of the 16-lane segment
                 auto xhalo = [&](const E (&row)[NE], T (&hl)[R], T (&hh)[R]) {
@@ -355,7 +388,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 // contributions of arriving plane q = s - (L-1) R to output planes p = q - dz
                 static_for<0, 2 * R + 1>([&](auto dc) {
                     constexpr int dz = R - decltype(dc)::value;
-                    constexpr int slot = ROT ? R - dz : pmod(k - (L - 1) * R - dz, P);
+                    constexpr int slot = ROT ? R - dz : pmod(k - (L - 1) * DL - dz, P);
                     auto tap = [&](const E c, int dy, int dx, bool first) {
 #pragma unroll
                         for (int yy = 0; yy < VY; ++yy) {
@@ -406,11 +439,23 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                     }
                 });
             });
-            // ---- STORE level BT plane p = s - BT*R, compute region only ----------------------------
-            const int pi = si - BT * R;
+            if constexpr (SK) {
+                // completed planes of levels 1..b_T-1: pin (ring), then publish their halo rows for
+                // the next step's levels 2..b_T; the next step's barrier orders the exchange
+                const int wb = xb ^ 1;
+                static_for<1, BT>([&](auto lc) {
+                    constexpr int l = decltype(lc)::value;
+                    auto& done = acc[l - 1][pmod(k - (l - 1) * DL - R, P)];
+                    if (step_pin) pin(done, si - (l - 1) * DL - R);
+                    publish(xch + (size_t)(wb * (BT - 1) + (l - 1)) * K::XBUF, done);
+                });
+                xb = wb;
+            }
+            // ---- STORE level BT plane p = s - (BT-1) DL - R, compute region only --------------------
+            const int pi = si - (BT - 1) * DL - R;
             if (pi >= rp0 && pi < rp1) {
-                const int64_t p = s - (int64_t)BT * R;
-                const auto& fin = acc[BT - 1][ROT ? 0 : pmod(k - (BT - 1) * R - R, P)];
+                const int64_t p = s - (int64_t)(BT - 1) * DL - R;
+                const auto& fin = acc[BT - 1][ROT ? 0 : pmod(k - (BT - 1) * DL - R, P)];
                 T* op = dst + p * a.pz + (int64_t)gy0 * a.py + gx0;
 #pragma unroll
                 for (int yy = 0; yy < VY; ++yy) {
