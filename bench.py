@@ -237,12 +237,15 @@ def main():
     ap.add_argument("--bt", type=int, default=0, help="force b_T (0 = planner)")
     ap.add_argument("--vec", type=int, default=0)
     ap.add_argument("--h", type=int, default=0)
+    ap.add_argument("--direct", type=int, default=0, choices=[0, 1],
+                    help="1 = partial sums OFF: the non-associative direct-gather kernels (BASELINE config 4)")
+    ap.add_argument("--no-tune", action="store_true", help="planner model only (no measured top-5 pick)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-step-seconds", type=float, default=3.0)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--T", type=int, default=0, help="override the time-step count")
-    ap.add_argument("--suite", default="", help="comma list of workload names (or 'all2d', 'all3d', 'all') "
+    ap.add_argument("--suite", default="", help="comma list of workload names (or 'all2d', 'all3d', 'all', 'config4' = box2d2r partial sums on+off) "
                     "to run back to back at the planner's config; one JSON line each (not a driver line)")
     ap.add_argument("--bt-sweep", default="", help="with --suite: comma list of b_T values to force in turn")
     args = ap.parse_args()
@@ -263,13 +266,19 @@ def run_suite(args):
             sel += [w for w in WORKLOADS if w.endswith("-512")]
         if tok in WORKLOADS:
             sel.append(tok)
+        if tok == "config4":   # BASELINE config 4: box2d2r fp32, partial sums on vs off
+            sel += ["box2d2r-f32-16384", "box2d2r-f32-16384@direct"]
     seen = set()
     sel = [w for w in sel if not (w in seen or seen.add(w))]
+    if args.direct:
+        sel = [w if "@" in w else w + "@direct" for w in sel]
     bts = [int(b) for b in args.bt_sweep.split(",") if b] or [args.bt]
     for w in sel:
         for bt in bts:
             a = argparse.Namespace(**vars(args))
-            a.workload, a.bt, a.no_cpu_baseline, a.no_e2e = w, bt, True, True
+            a.workload, a.bt, a.no_cpu_baseline, a.no_e2e = w.split("@")[0], bt, True, True
+            if w.endswith("@direct"):
+                a.direct = 1
             try:
                 run_an5d(a)
             except Exception as e:  # report and continue (e.g. no instance for a forced b_T)
@@ -298,11 +307,18 @@ def run_an5d(args):
     ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
     ext = (n + 2 * rad,) * ndim
     st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
-    cfg = st.plan_config(ext, T, {"bT": args.bt, "vec": args.vec, "h": args.h})
-    geom = st.describe(ext, cfg)
+    hint = {"bT": args.bt, "vec": args.vec, "h": args.h, "direct": args.direct}
     a = an5d.empty_grid(ext, rad, dtype, dev)
     b = an5d.empty_grid(ext, rad, dtype, dev)
     fill_uniform(a, inputs.DEFAULT_SEED, ext)
+    # planner: the model's top 5 (b_T, vec) candidates run once each, fastest kept;
+    # untimed, before the warm-up
+    if args.no_tune:
+        cfg = st.plan_config(ext, T, hint)
+    else:
+        cfg = st.tune(a, b, T, hint, top_k=5)
+        cfg.pop("seconds_per_cell_step", None)
+    geom = st.describe(ext, cfg)
     b.copy_(a)
     stream = torch.cuda.current_stream(dev)
     bufs = [a, b]
@@ -360,7 +376,8 @@ def run_an5d(args):
         rl = {"bound": "alu", "achieved": round(achieved, 2), "peak": round(fp_peak / 1e12, 2), "unit": "TFLOP/s",
               "frac": round(achieved * 1e12 / fp_peak, 4)}
     rl["traffic"] = _traffic(args.workload, cfg)
-    rl["kernel"] = f"an5d_sweep{ndim}d<{dtype_name},R={rad},bT={cfg['bT']},vec={cfg['vec']}> (interior+edge)"
+    rl["kernel"] = (f"an5d_sweep{ndim}d<{dtype_name},R={rad},bT={cfg['bT']},vec={cfg['vec']}"
+                    f"{',direct' if cfg.get('direct') else ''}> (interior+edge)")
     rl["sweep_ms"] = round(sweep_avg, 4)
     rl["alg_bytes_per_launch"] = alg_bytes
     rl["alg_flops_per_launch"] = alg_flops
@@ -410,7 +427,9 @@ def run_an5d(args):
         "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if dtype == torch.float32 else "f64", "data": "synthetic",
         "config": {"workload": args.workload, "stencil": name, "grid": list(ext), "T": T, "bT": cfg["bT"],
-                   "vec": cfg["vec"], "h": cfg["h"], "bS": geom["bS"][:nb], "bS_loaded": geom["bS_loaded"][:nb],
+                   "vec": cfg["vec"], "h": cfg["h"], "partial_sums": "off" if cfg.get("direct") else "on",
+                   "planner": "model" if args.no_tune else "model top-5, measured pick (P:784-793)",
+                   "bS": geom["bS"][:nb], "bS_loaded": geom["bS_loaded"][:nb],
                    "parallelism": "1 GPU", "l2": "inputs larger than L2 (1 GiB per grid buffer > 126 MB)",
                    "regs_per_thread": geom["regs_per_thread"]},
         "gflops": round(gcells * F, 2),

@@ -67,6 +67,12 @@ typedef struct {
                      /* b_S_x rounded up so that halos are whole 16-byte vectors.    */
     int64_t h;       /* stream-block length h_SN along the streaming dimension       */
     int vec;         /* cells per thread along y (3D) or x (2D): register tiling factor V        */
+    int direct;      /* 0: associative partial sums (the default for both   */
+                     /*    shapes).  1: the non-associative "Otherwise" variant of Table 1       */
+                     /*    (P:262-270): each level gathers an output from its 2*rad+1 input rows */
+                     /*    at once -- kept for the partial-sum on/off comparison (BASELINE       */
+                     /*    config 4).  2D only (else AN5D_ERR_UNSUPPORTED); the planner never    */
+                     /*    picks 1 by itself.  Values other than 0/1: AN5D_ERR_INVALID_ARGUMENT. */
 } an5d_config;
 
 /* Bookkeeping of one sweep of degree bT under `cfg` (bit-exact).        */
@@ -135,6 +141,19 @@ an5d_status an5d_copy_ring(an5d_plan* plan, const void* src, void* dst, const in
  * DESIGN.md "Planner"); fields of `hint` that are non-zero are kept.                            */
 an5d_status an5d_plan_config(an5d_plan* plan, const int64_t* extents, int64_t T,
                              const an5d_config* hint, an5d_config* out);
+
+/* Tuned configuration (the paper's procedure): rank every configuration with the
+ * model of an5d_plan_config, run the best stream-block length of each of the top_k distinct
+ * (bT, vec) pairs on the device and return the fastest (measured over two sweeps after a warm-up
+ * sweep).  Non-zero fields of `hint` are kept, as in an5d_plan_config.
+ *   grid_in: read only.  grid_out: overwritten (interior) -- pass the buffers of the following
+ *   an5d_run, which rewrites grid_out entirely.  Same extents/pitches/alignment rules as an5d_run.
+ *   best_seconds_per_cell_step: optional (NULL); the winner's measured time per cell and step.
+ *   Synchronises cuda_stream (a blocking host call; do it once, outside any timed region).
+ *   Errors: as an5d_run; AN5D_ERR_CUDA if no candidate could run.                              */
+an5d_status an5d_tune(an5d_plan* plan, const void* grid_in, void* grid_out, const int64_t* extents,
+                      const int64_t* pitches, int64_t T, const an5d_config* hint, int top_k,
+                      an5d_config* out, double* best_seconds_per_cell_step, void* cuda_stream);
 
 /* Bookkeeping introspection for one sweep of degree cfg->bT (bit-exact tests).                 */
 an5d_status an5d_describe(an5d_plan* plan, const int64_t* extents, const an5d_config* cfg,

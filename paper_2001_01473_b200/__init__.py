@@ -32,10 +32,11 @@ class AN5DError(RuntimeError):
 
 
 class Config(ctypes.Structure):
-    _fields_ = [("bT", ctypes.c_int), ("bS", ctypes.c_int * 2), ("h", ctypes.c_int64), ("vec", ctypes.c_int)]
+    _fields_ = [("bT", ctypes.c_int), ("bS", ctypes.c_int * 2), ("h", ctypes.c_int64), ("vec", ctypes.c_int),
+                ("direct", ctypes.c_int)]
 
     def as_dict(self):
-        return {"bT": self.bT, "bS": list(self.bS), "h": self.h, "vec": self.vec}
+        return {"bT": self.bT, "bS": list(self.bS), "h": self.h, "vec": self.vec, "direct": self.direct}
 
 
 class Geometry(ctypes.Structure):
@@ -71,6 +72,8 @@ def _load():
         "an5d_copy_ring": (I32, [P, P, P, pi64, pi64, I64, I64, P]),
         "an5d_plan_config": (I32, [P, pi64, I64, ctypes.POINTER(Config), ctypes.POINTER(Config)]),
         "an5d_describe": (I32, [P, pi64, ctypes.POINTER(Config), ctypes.POINTER(Geometry)]),
+        "an5d_tune": (I32, [P, P, P, pi64, pi64, I64, ctypes.POINTER(Config), I32, ctypes.POINTER(Config),
+                            ctypes.POINTER(ctypes.c_double), P]),
         "an5d_schedule": (I32, [I64, I32, ctypes.POINTER(ctypes.c_int), I64, pi64, ctypes.POINTER(ctypes.c_int)]),
         "an5d_last_launch_count": (I64, [P]),
         "an5d_destroy": (I32, [P]),
@@ -85,7 +88,7 @@ def _load():
 
 
 _lib = _load()
-EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_copy_ring", "an5d_plan_config",
+EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
                     "an5d_describe", "an5d_schedule", "an5d_last_launch_count", "an5d_destroy",
                     "an5d_last_error", "an5d_version")
 
@@ -112,6 +115,7 @@ def _cfg(cfg) -> Config | None:
     c.bS[1] = int(bs[1]) if len(bs) > 1 else 0
     c.h = int(cfg.get("h", 0))
     c.vec = int(cfg.get("vec", 0))
+    c.direct = int(cfg.get("direct", 0))
     return c
 
 
@@ -237,6 +241,23 @@ class Stencil:
         _check(_lib.an5d_plan_config(self._h, _i64(extents), int(T), ctypes.byref(h) if h else None,
                                      ctypes.byref(out)))
         return out.as_dict()
+
+    def tune(self, grid_in: torch.Tensor, grid_out: torch.Tensor, T: int = 0, hint=None, top_k: int = 5,
+             stream=None) -> dict:
+        """Model top-k + measured pick (an5d_tune).  Reads grid_in, overwrites grid_out's
+        interior; blocks until the candidate sweeps are timed.  Returns the config with the measured
+        "seconds_per_cell_step" of the winner."""
+        ext, pit = _geom_of(grid_in)
+        st = stream if stream is not None else torch.cuda.current_stream(grid_in.device)
+        out = Config()
+        best = ctypes.c_double()
+        h = _cfg(hint)
+        _check(_lib.an5d_tune(self._h, grid_in.data_ptr(), grid_out.data_ptr(), _i64(ext), _i64(pit), int(T),
+                              ctypes.byref(h) if h else None, int(top_k), ctypes.byref(out), ctypes.byref(best),
+                              ctypes.c_void_p(st.cuda_stream)))
+        d = out.as_dict()
+        d["seconds_per_cell_step"] = best.value
+        return d
 
     def describe(self, extents, cfg) -> dict:
         out = Geometry()

@@ -1,6 +1,7 @@
 // an5d_host.cu -- libAN5D host side: C ABI (include/an5d.h), sweep geometry, sweep schedule,
 // B200 planner, launch orchestration.  Product code: shares nothing with oracle/.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no libcuda link)
 
 #include <algorithm>
 #include <cmath>
@@ -95,10 +96,10 @@ void make_schedule(int64_t T, int bT, std::vector<int>& deg, bool& trailing_copy
     }
 }
 
-const Instance* find_instance(const Plan& p, int bT, int vec) {
+const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0) {
     for (const Instance& i : registry())
         if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad &&
-            i.bT == bT && i.vec == vec)
+            i.bT == bT && i.vec == vec && i.assoc == (direct ? 0 : 1))
             return &i;
     return nullptr;
 }
@@ -285,31 +286,32 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     return t / ((double)interior * bT);
 }
 
-an5d_status choose_config(const Plan& p, const Dims& dm, int64_t T, const an5d_config* hint, an5d_config& out) {
+// Every feasible configuration with its model time (seconds per cell-step), best first.
+std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Dims& dm, int64_t T,
+                                                         const an5d_config* hint) {
     const DevInfo di = dev_info();
-    double best = 1e300;
-    an5d_config bc{};
+    std::vector<std::pair<double, an5d_config>> out;
     const int64_t Iout = dm.E[0] - 2 * p.rad;
     for (const Instance& inst : registry()) {
         if (inst.ndim != p.ndim || inst.shape != p.shape || inst.dtype != p.dtype || inst.rad != p.rad) continue;
+        const int direct = hint ? hint->direct : 0;
+        if (inst.assoc != (direct ? 0 : 1)) continue;
         if (hint && hint->bT && inst.bT != hint->bT) continue;
         if (hint && hint->vec && inst.vec != hint->vec) continue;
         if (T > 0 && inst.bT > T) continue;
         // every reduced degree the schedule may need must exist with the same vec
         bool ok = true;
-        for (int d = 1; d < inst.bT && ok; ++d) ok = find_instance(p, d, inst.vec) != nullptr;
+        for (int d = 1; d < inst.bT && ok; ++d) ok = find_instance(p, d, inst.vec, direct) != nullptr;
         if (!ok) continue;
         std::vector<int64_t> hs;
         if (hint && hint->h) {
             hs.push_back(hint->h);
         } else {
-            // candidate stream-block lengths: 1..4 waves of resident units
             SweepGeom g{};
             if (sweep_geometry(p, inst, dm, inst.bT, Iout, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g) != AN5D_OK) continue;
             int64_t nt = 1;
             for (int i = 0; i < p.ndim - 1; ++i) nt *= g.ntiles[i];
-            const int per_sm = resident_blocks(inst) * 1;
-            const int64_t conc = (int64_t)per_sm * di.n_sm;
+            const int64_t conc = (int64_t)resident_blocks(inst) * di.n_sm;
             // stream-block lengths giving 1..32 units per resident block, and a few fixed lengths
             for (int w : {1, 2, 4, 8, 16, 32}) {
                 const int64_t nsb = std::max<int64_t>(1, (w * conc) / std::max<int64_t>(1, nt));
@@ -320,18 +322,25 @@ an5d_status choose_config(const Plan& p, const Dims& dm, int64_t T, const an5d_c
         }
         for (int64_t h : hs) {
             const double t = model_time(p, inst, dm, inst.bT, h, di, nullptr);
-            if (t < best) {
-                best = t;
-                bc.bT = inst.bT;
-                bc.vec = inst.vec;
-                bc.h = h;
-            }
+            if (t >= 1e29) continue;
+            an5d_config c{};
+            c.bT = inst.bT;
+            c.vec = inst.vec;
+            c.h = h;
+            c.direct = direct;
+            out.emplace_back(t, c);
         }
     }
-    if (best >= 1e29)
+    std::stable_sort(out.begin(), out.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    return out;
+}
+
+an5d_status choose_config(const Plan& p, const Dims& dm, int64_t T, const an5d_config* hint, an5d_config& out) {
+    const auto r = rank_configs(p, dm, T, hint);
+    if (r.empty())
         return fail(AN5D_ERR_UNSUPPORTED, "no feasible kernel instance for ndim=%d rad=%d shape=%d dtype=%d",
                     p.ndim, p.rad, p.shape, p.dtype);
-    out = bc;
+    out = r.front().second;
     return AN5D_OK;
 }
 
@@ -419,11 +428,44 @@ an5d_status ensure_streams(Plan& p) {
     return AN5D_OK;
 }
 
+// The TMA descriptor of a 3D sweep's input: the local array as a tensor {x, y, z} whose origin is
+// moved back to the 16-byte boundary before x = 0 (TMA needs a 16-byte aligned base; the C ABI
+// guarantees (base + rad*elem) % 16 == 0, so that boundary lies at most 12 bytes before the array
+// inside the same allocation).  Box = one staged tile plane {kTX, kTY, 1}; out-of-bound parts
+// (y < 0, y >= E_y, z outside the local array, x past the row end) are zero-filled by the TMA unit.
+an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src, const Dims& dm, CUtensorMap& tm,
+                           int& x_off) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f) {
+            cudaGetLastError();
+            return fail(AN5D_ERR_CUDA, "cuTensorMapEncodeTiled entry point not available");
+        }
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    const uintptr_t base = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t aligned = base & ~uintptr_t(15);
+    x_off = (int)((base - aligned) / p.elem);
+    const cuuint64_t dims[3] = {(cuuint64_t)(dm.E[2] + x_off), (cuuint64_t)dm.E[1], (cuuint64_t)dm.E[0]};
+    const cuuint64_t strides[2] = {(cuuint64_t)(dm.pitch[1] * p.elem), (cuuint64_t)(dm.pitch[0] * p.elem)};
+    const cuuint32_t box[3] = {(cuuint32_t)inst.tile_x_loaded, (cuuint32_t)inst.tile_y, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(&tm, p.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                        reinterpret_cast<void*>(aligned), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(AN5D_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return AN5D_OK;
+}
+
 // One sweep: edge units on the side stream, interior units on the caller's stream, joined.
 an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, int d, const an5d_config& cfg,
                          int64_t g_off, int64_t gE0, int64_t out_lo, int64_t out_hi, int32_t* wc,
                          cudaStream_t st) {
-    const Instance* inst = find_instance(p, d, cfg.vec);
+    const Instance* inst = find_instance(p, d, cfg.vec, cfg.direct);
     if (!inst) return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for degree %d vec %d", d, cfg.vec);
     SweepGeom g{};
     an5d_status s = sweep_geometry(p, *inst, dm, d, cfg.h, g_off, gE0, out_lo, out_hi, g);
@@ -469,7 +511,9 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.Ey = (int)dm.E[1]; a.Ex = (int)dm.E[2];
         a.Cy = g.C[0]; a.Cx = g.C[1]; a.Hy = g.halo[0]; a.Hx = g.halo[1];
         a.nty = (int)g.ntiles[0]; a.ntx = (int)g.ntiles[1];
-        if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), g.n_units, false, st)) != cudaSuccess)
+        CUtensorMap tm;
+        if ((s = encode_tmap_3d(p, *inst, src, dm, tm, a.x_off)) != AN5D_OK) return s;
+        if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), tm, g.n_units, st)) != cudaSuccess)
             return cuda_fail(e, "sweep launch");
         p.launches++;
     }
@@ -521,20 +565,23 @@ an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config
         }
     }
     if (hint.bT < 0 || hint.vec < 0 || hint.h < 0) return fail(AN5D_ERR_INVALID_ARGUMENT, "negative config field");
+    if (hint.direct != 0 && hint.direct != 1) return fail(AN5D_ERR_INVALID_ARGUMENT, "direct must be 0 or 1");
     if (hint.bT && hint.vec && hint.h) {
         c = hint;
     } else {
         an5d_status s = choose_config(p, dm, T, &hint, c);
         if (s != AN5D_OK) return s;
     }
-    if (!find_instance(p, c.bT, c.vec))
+    if (c.direct && p.ndim != 2)
+        return fail(AN5D_ERR_UNSUPPORTED, "direct (non-associative) variant is 2D only");
+    if (!find_instance(p, c.bT, c.vec, c.direct))
         return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for ndim=%d rad=%d shape=%d dtype=%d bT=%d vec=%d",
                     p.ndim, p.rad, p.shape, p.dtype, c.bT, c.vec);
     for (int d = 1; d < c.bT; ++d)
-        if (!find_instance(p, d, c.vec))
+        if (!find_instance(p, d, c.vec, c.direct))
             return fail(AN5D_ERR_UNSUPPORTED, "no reduced-degree instance d=%d for vec %d", d, c.vec);
     // logical tile b_S reported back
-    const Instance* inst = find_instance(p, c.bT, c.vec);
+    const Instance* inst = find_instance(p, c.bT, c.vec, c.direct);
     SweepGeom g{};
     an5d_status s = sweep_geometry(p, *inst, dm, c.bT, c.h ? c.h : dm.E[0], 0, dm.E[0], p.rad, dm.E[0] - p.rad, g);
     if (s != AN5D_OK) return s;
@@ -653,6 +700,82 @@ an5d_status an5d_plan_config(an5d_plan* p, const int64_t* extents, int64_t T, co
     }
 }
 
+// The paper's tuning procedure: rank every configuration with the model, run the top
+// few on the GPU, keep the fastest.  Candidates are the best stream-block length of each of the
+// top_k distinct (b_T, vec) pairs; each is timed over two sweeps (after one warm-up sweep) reading
+// grid_in and writing grid_out.  Blocking: synchronises cuda_stream.
+an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const int64_t* extents,
+                      const int64_t* pitches, int64_t T, const an5d_config* hint, int top_k, an5d_config* out,
+                      double* best_seconds_per_cell_step, void* stream) {
+    try {
+        if (!p || !out || !grid_in || !grid_out) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (top_k < 1) return fail(AN5D_ERR_INVALID_ARGUMENT, "top_k < 1");
+        if (grid_in == grid_out) return fail(AN5D_ERR_INVALID_ARGUMENT, "grid_in and grid_out must differ");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, pitches, dm);
+        if (s != AN5D_OK) return s;
+        if ((s = check_alignment(*p, grid_in, dm, "grid_in")) != AN5D_OK) return s;
+        if ((s = check_alignment(*p, grid_out, dm, "grid_out")) != AN5D_OK) return s;
+        an5d_config h{};
+        if (hint) h = *hint;
+        if (h.bT < 0 || h.vec < 0 || h.h < 0 || (h.direct != 0 && h.direct != 1))
+            return fail(AN5D_ERR_INVALID_ARGUMENT, "bad hint");
+        const auto ranked = rank_configs(*p, dm, T, &h);
+        std::vector<an5d_config> cand;
+        for (const auto& r : ranked) {
+            bool seen = false;
+            for (const auto& c : cand) seen = seen || (c.bT == r.second.bT && c.vec == r.second.vec);
+            if (!seen) cand.push_back(r.second);
+            if ((int)cand.size() >= top_k) break;
+        }
+        if (cand.empty())
+            return fail(AN5D_ERR_UNSUPPORTED, "no feasible kernel instance for ndim=%d rad=%d shape=%d dtype=%d",
+                        p->ndim, p->rad, p->shape, p->dtype);
+        if ((s = ensure_streams(*p)) != AN5D_OK) return s;
+        cudaStream_t st = (cudaStream_t)stream;
+        cudaEvent_t e0, e1;
+        cudaError_t e;
+        if ((e = cudaEventCreate(&e0)) != cudaSuccess) return cuda_fail(e, "event");
+        if ((e = cudaEventCreate(&e1)) != cudaSuccess) { cudaEventDestroy(e0); return cuda_fail(e, "event"); }
+        int64_t interior = 1;
+        for (int i = 0; i < p->ndim; ++i) interior *= dm.E[i] - 2 * p->rad;
+        double best = 1e300;
+        an5d_config bc{};
+        const int64_t launches0 = p->launches;
+        for (const an5d_config& c0 : cand) {
+            an5d_config c{};
+            if (resolve_config(*p, dm, T, &c0, c) != AN5D_OK) continue;
+            bool ok = launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
+                                   nullptr, st) == AN5D_OK;
+            cudaEventRecord(e0, st);
+            for (int r = 0; r < 2 && ok; ++r)
+                ok = launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
+                                  nullptr, st) == AN5D_OK;
+            cudaEventRecord(e1, st);
+            if (cudaEventSynchronize(e1) != cudaSuccess || !ok) {
+                cudaGetLastError();
+                continue;
+            }
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double t = ms * 1e-3 / 2.0 / ((double)interior * c.bT);
+            if (t < best) {
+                best = t;
+                bc = c;
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        p->launches = launches0;
+        if (best >= 1e299) return fail(AN5D_ERR_CUDA, "no candidate configuration ran");
+        *out = bc;
+        if (best_seconds_per_cell_step) *best_seconds_per_cell_step = best;
+        return AN5D_OK;
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
 an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_config* cfg, an5d_geometry* out) {
     try {
         if (!p || !out || !cfg) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
@@ -661,7 +784,7 @@ an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_confi
         if (s != AN5D_OK) return s;
         an5d_config c{};
         if ((s = resolve_config(*p, dm, 0, cfg, c)) != AN5D_OK) return s;
-        const Instance* inst = find_instance(*p, c.bT, c.vec);
+        const Instance* inst = find_instance(*p, c.bT, c.vec, c.direct);
         SweepGeom g{};
         if ((s = sweep_geometry(*p, *inst, dm, c.bT, c.h, 0, dm.E[0], p->rad, dm.E[0] - p->rad, g)) != AN5D_OK)
             return s;
@@ -766,7 +889,7 @@ an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t*
         make_schedule(T, c.bT, deg, tc);
         // validate every sweep's geometry before the first launch (no partial writes on error)
         for (int d : deg) {
-            const Instance* inst = find_instance(*p, d, c.vec);
+            const Instance* inst = find_instance(*p, d, c.vec, c.direct);
             SweepGeom g{};
             if ((s = sweep_geometry(*p, *inst, dm, d, c.h, 0, dm.E[0], p->rad, dm.E[0] - p->rad, g)) != AN5D_OK)
                 return s;

@@ -1,0 +1,45 @@
+// inst2d.cuh -- launcher and registry entry of one 2D kernel instance (included by the generated
+// csrc/gen/inst_2d_*.cu files only, so a 2D change does not rebuild the 3D instances).
+#pragma once
+#include "kernel2d.cuh"
+#include "registry.hpp"
+
+namespace an5d {
+
+template <typename T, int R, int BT, int V, bool BOX, bool ASSOC>
+cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, bool /*edge*/,
+                     cudaStream_t st) {
+    Coeffs2D<T, R> cf;
+    const T* c = static_cast<const T*>(coeffs);
+    for (int i = 0; i < (2 * R + 1) * (2 * R + 1); ++i) {
+        if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
+        else cf.c[i] = c[i];
+    }
+    constexpr size_t smem = smem_bytes_2d<T, R, BT, V, ASSOC>();
+    auto fn = &an5d_sweep2d<T, R, BT, V, BOX, ASSOC>;
+    static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
+    if (smem > 48 * 1024 && !attr_set) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    fn<<<(unsigned)blocks, 32, smem, st>>>(a, cf);
+    return cudaGetLastError();
+}
+
+template <typename T, int R, int BT, int V, bool BOX, bool ASSOC = true>
+Instance make_instance2d() {
+    Instance i{};
+    i.ndim = 2; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
+    i.rad = R; i.bT = BT; i.vec = V; i.assoc = ASSOC ? 1 : 0;
+    i.launch2d = &launch2d<T, R, BT, V, BOX, ASSOC>;
+    i.launch3d = nullptr;
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, ASSOC>);
+    i.fn_edge = i.fn_interior;
+    i.threads = 32;
+    i.tile_x_loaded = 32 * V;
+    i.tile_y = 0;
+    i.smem_bytes = smem_bytes_2d<T, R, BT, V, ASSOC>();
+    return i;
+}
+
+}  // namespace an5d

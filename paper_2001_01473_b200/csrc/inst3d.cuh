@@ -1,0 +1,47 @@
+// inst3d.cuh -- launcher and registry entry of one 3D kernel instance (included by the generated
+// csrc/gen/inst_3d_*.cu files only).
+#pragma once
+#include "kernel3d.cuh"
+#include "registry.hpp"
+
+namespace an5d {
+
+template <typename T, int R, int BT, int VY, bool BOX>
+cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap& tmap, int64_t blocks,
+                     cudaStream_t st) {
+    using K = Kernel3DTraits<T, R, BT, VY>;
+    constexpr int N = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
+    Coeffs3D<T, R> cf;
+    const T* c = static_cast<const T*>(coeffs);
+    for (int i = 0; i < N; ++i) {
+        if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
+        else cf.c[i] = c[i];
+    }
+    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX>;
+    static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
+    if (!attr_set) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
+        attr_set = true;
+    }
+    fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf, tmap);
+    return cudaGetLastError();
+}
+
+template <typename T, int R, int BT, int VY, bool BOX>
+Instance make_instance3d() {
+    using K = Kernel3DTraits<T, R, BT, VY>;
+    Instance i{};
+    i.ndim = 3; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
+    i.rad = R; i.bT = BT; i.vec = VY; i.assoc = 1;
+    i.launch2d = nullptr;
+    i.launch3d = &launch3d<T, R, BT, VY, BOX>;
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX>);
+    i.fn_edge = i.fn_interior;
+    i.threads = K::kThreads;
+    i.tile_x_loaded = K::kTX;
+    i.tile_y = K::kTY;
+    i.smem_bytes = K::kSmemBytes;
+    return i;
+}
+
+}  // namespace an5d

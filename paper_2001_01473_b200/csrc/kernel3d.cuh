@@ -24,33 +24,20 @@
 //     neighbours: own registers + rad rows from the threads above / below through shared memory;
 //   * fp32 arithmetic in packed pairs (FFMA2/FMUL2) for every tap with an even x offset, scalar
 //     FFMA for odd x offsets (see lane.cuh);
-//   * level-0 planes staged by cp.async into a ring of D planes (prefetch distance PF, plus the
-//     (b_T-1)*rad planes ring pinning reads back);
+//   * level-0 planes staged by TMA (cp.async.bulk.tensor.3d, one elected thread, completion on one
+//     mbarrier per stage slot) into a ring of D planes (prefetch distance PF, plus the (b_T-1)*rad
+//     planes ring pinning reads back).  The hardware zero-fills the parts of the tile window that
+//     leave the array (y, z, x past the end), so edge tiles stage exactly like interior ones;
 //   * one block per (tile, stream block) unit; units whose tile window touches the x/y ring or the
 //     array end are numbered first and run a separately instantiated EDGE copy of the stream loop
 //     (the z ring / z array ends cost a uniform per-step check in both copies).
 #pragma once
+#include "args.hpp"
 #include "common.cuh"
 #include "lane.cuh"
 
 namespace an5d {
 
-struct Sweep3DArgs {
-    const void* src;
-    void* dst;
-    int64_t pz, py;          // plane and row strides (elements)
-    int64_t Ez;              // local planes
-    int64_t g_off, gEz;      // global index of local plane 0, global z extent (slab mode)
-    int64_t out_lo, out_hi;  // local output planes [out_lo, out_hi)
-    int64_t h;               // stream-block length
-    int64_t n_units;         // units of this sweep (= blocks)
-    int64_t n_sb;            // stream blocks
-    int32_t* wc;             // debug store counts (dense Ez x Ey x Ex) or nullptr
-    int Ey, Ex;
-    int Cy, Cx;              // compute region per tile
-    int Hy, Hx;              // loaded halo per side (Hy = degree*rad; Hx rounded to 16 bytes)
-    int nty, ntx;            // tiles along y, x
-};
 
 constexpr int kPrefetch3D = 3;
 
@@ -76,7 +63,10 @@ struct Kernel3DTraits {
     // rotated-slot kernels and where the shared memory would not fit.
     static constexpr int D0 = kPrefetch3D + (BT - 1) * R + 1;                       // SK = 0
     static constexpr int D1 = kPrefetch3D + (BT >= 2 ? (BT - 2) * (R + 1) + R : 0) + 1;  // SK = 1
-    static constexpr size_t smem_of(int d, int nxb) { return ((size_t)d * PLANE + (size_t)nxb * XBUF) * sizeof(T); }
+    // D staged planes, nxb exchange buffers, D mbarriers (one per stage slot)
+    static constexpr size_t smem_of(int d, int nxb) {
+        return ((size_t)d * PLANE + (size_t)nxb * XBUF) * sizeof(T) + (size_t)d * 8;
+    }
     static constexpr size_t kSmem1 = smem_of(D1, 2 * (BT - 1));
 #ifndef AN5D_SK3D
     static constexpr int SK = (BT >= 2 && kSmem1 <= 220 * 1024) ? 1 : 0;
@@ -139,7 +129,7 @@ using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * 
 
 template <typename T, int R, int BT, int VY, bool BOX, bool EDGE>
 __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
-                                             const Unit3D& g) {
+                                             const Unit3D& g, const void* tmap) {
     using K = Kernel3DTraits<T, R, BT, VY>;
     using LN = Lane<T, K::VX>;
     using E = typename LN::E;
@@ -160,7 +150,6 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     constexpr int DL = R + SK;              // plane delay per level
     constexpr int kTX = K::kTX;
 
-    const T* __restrict__ src = static_cast<const T*>(a.src);
     T* __restrict__ dst = static_cast<T*>(a.dst);
     const int tid = threadIdx.x;
     const int txi = tid % K::TXT, tyi = tid / K::TXT;
@@ -170,8 +159,8 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     T* const xch = smem + (size_t)D * K::PLANE;         // 2 exchange buffers
     const int own = (ys + R) * kTX + xs;                // patch origin inside a staged plane
 
-    // per-thread masks (EDGE): loadable vectors, ring cells, store coverage
-    unsigned ld_ok = 0, ring_mask = 0, st_full = 0, st_elem = 0;
+    // per-thread masks (EDGE): ring cells, store coverage
+    unsigned ring_mask = 0, st_full = 0, st_elem = 0;
 #pragma unroll
     for (int yy = 0; yy < VY; ++yy) {
         const int y = gy0 + yy;
@@ -179,7 +168,6 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
             const int x = gx0 + j * A;
-            if (!EDGE || (yin && x >= 0 && x + A <= a.Ex)) ld_ok |= 1u << (yy * NCH + j);
             if (y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x + A <= g.cx1) st_full |= 1u << (yy * NCH + j);
         }
         if constexpr (EDGE) {
@@ -195,39 +183,26 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
         }
     }
 
-    // ---- level-0 staging ------------------------------------------------------------------------
+    // ---- level-0 staging: one TMA box {kTX, kTY, 1} per plane, issued by thread 0 -------------------
+    // Planes outside [s_a, s_b) are not loaded (they feed nothing that is stored or pinned): the
+    // slot's barrier is completed by a plain arrive.
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(smem + (size_t)D * K::PLANE + (size_t)K::NXB * K::XBUF);
+    constexpr unsigned kBoxBytes = (unsigned)(K::kTX * K::kTY * sizeof(T));
     auto issue_plane = [&](int64_t q, int slot) {
-        T* sl = stage + (size_t)slot * K::PLANE + own;
-        if (q >= g.s_a && q < g.s_b) {
-            const T* gp = src + q * a.pz + (int64_t)gy0 * a.py + gx0;
-#pragma unroll
-            for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                for (int j = 0; j < NCH; ++j) {
-                    if constexpr (!EDGE) {
-                        cp_async16(sl + yy * kTX + j * A, gp + yy * a.py + j * A, 16);
-                    } else {
-                        const bool full = (ld_ok >> (yy * NCH + j)) & 1u;
-                        cp_async16_pred(sl + yy * kTX + j * A, full ? gp + yy * a.py + j * A : src + R, 16, full);
-                        const int y = gy0 + yy;
-                        const bool yin = y >= 0 && y < a.Ey;
-#pragma unroll
-                        for (int e = 0; e < A; ++e) {
-                            const int x = gx0 + j * A + e;
-                            const bool in = yin && x >= 0 && x < a.Ex;
-                            cp_async_elem_pred<sizeof(T)>(sl + yy * kTX + j * A + e,
-                                                          in ? gp + yy * a.py + j * A + e : src + R,
-                                                          in ? (int)sizeof(T) : 0, !full);
-                        }
-                    }
-                }
-        } else {
-#pragma unroll
-            for (int yy = 0; yy < VY; ++yy)
-#pragma unroll
-                for (int j = 0; j < NCH; ++j) cp_async16(sl + yy * kTX + j * A, src + R, 0);
+        if (tid == 0) {
+            if (q >= g.s_a && q < g.s_b) {
+                mbar_arrive_expect_tx(mbar + slot, kBoxBytes);
+                tma_load_3d(stage + (size_t)slot * K::PLANE + R * kTX, tmap, g.wx0 + a.x_off, g.wy0, (int)q,
+                            mbar + slot);
+            } else {
+                mbar_arrive(mbar + slot);
+            }
         }
-        cp_async_commit();
+    };
+    unsigned phase = 0;   // bit d: parity of the next completion of slot d's barrier
+    auto wait_plane = [&](int slot) {
+        mbar_wait(mbar + slot, (phase >> slot) & 1u);
+        phase ^= 1u << slot;
     };
     // a patch row (VX cells) of a staged/exchange row pointer -> elements
     auto load_row = [&](E (&P_)[NE], const T* p) {
@@ -261,6 +236,11 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     const int rlo = rel((int64_t)R - a.g_off), rhi = rel(a.gEz - R - a.g_off);
     const int rp0 = rel(g.p0), rp1 = rel(g.p1);
 
+    if (tid == 0) {
+        for (int d = 0; d < D; ++d) mbar_init(mbar + d, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
 #pragma unroll
     for (int d = 0; d < PF; ++d) issue_plane(base0 + d, d);
 
@@ -319,12 +299,12 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             constexpr int k = decltype(kc)::value;
             const int64_t s = base + k;
             const int si = i;
-            cp_async_wait<PF - 1>();
-            __syncthreads();                                   // plane s visible to every thread
+            wait_plane(slot_i);                                // plane s has landed (TMA, mbarrier)
+            __syncthreads();                                   // ... and every thread is past step s-1
             {
                 int ns = slot_i + PF;
                 if (ns >= D) ns -= D;
-                issue_plane(s + PF, ns);   // planes outside [s_a, s_b) are zero-filled, no traffic
+                issue_plane(s + PF, ns);   // planes outside [s_a, s_b): no traffic
             }
             const T* cur = stage + (size_t)slot_i * K::PLANE;
             ++i;
@@ -494,19 +474,30 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             }
         });
     }
-    cp_async_wait<0>();
+    // drain: the PF planes still in flight must land before the block's shared memory is released
+#pragma unroll
+    for (int d = 0; d < PF; ++d) {
+        wait_plane(slot_i);
+        if (++slot_i == D) slot_i = 0;
+    }
 }
 
 // resident blocks per SM the register budget is shaped for: small fp32 patches (VY <= 2) fit two
 // blocks (<= 128 registers/thread), so one block's barrier and latency stalls overlap the other's;
 // fp64 (twice the registers per cell) and high-order box keep one block and up to 255 registers
+// (build.py lowers the cap with AN5D_MINB_CAP when ptxas reports spills at 128 registers)
 template <typename T, int VY, int R, bool BOX> constexpr int min_blocks_3d() {
-    return (sizeof(T) == 4 && VY <= 2 && !(BOX && R >= 2)) ? 2 : 1;
+    constexpr int m = (sizeof(T) == 4 && VY <= 2 && !(BOX && R >= 2)) ? 2 : 1;
+#ifdef AN5D_MINB_CAP
+    return m < AN5D_MINB_CAP ? m : AN5D_MINB_CAP;
+#else
+    return m;
+#endif
 }
 
 template <typename T, int R, int BT, int VY, bool BOX>
 __global__ void __launch_bounds__(256, min_blocks_3d<T, VY, R, BOX>())
-an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf) {
+an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
     using K = Kernel3DTraits<T, R, BT, VY>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* const smem = reinterpret_cast<T*>(smem_raw);
@@ -531,8 +522,9 @@ an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf) {
     g.ring_xy = g.wy0 < R || g.wy0 + K::kTY > a.Ey - R || g.wx0 < R || g.wx0 + K::kTX > a.Ex - R;
     // z-ring planes and the array's z ends are handled by both variants (uniform per-step checks);
     // the EDGE variant is only for tiles whose window touches the x/y ring or the array end
-    if (g.ring_xy) sweep3d_unit<T, R, BT, VY, BOX, true>(a, cf, smem, g);
-    else sweep3d_unit<T, R, BT, VY, BOX, false>(a, cf, smem, g);
+    if (threadIdx.x == 0) tma_prefetch_desc(&tmap);
+    if (g.ring_xy) sweep3d_unit<T, R, BT, VY, BOX, true>(a, cf, smem, g, &tmap);
+    else sweep3d_unit<T, R, BT, VY, BOX, false>(a, cf, smem, g, &tmap);
 }
 
 }  // namespace an5d

@@ -47,7 +47,7 @@ def small_ext(ndim, rad):
     return (61 + 2 * rad, 411 + 2 * rad) if ndim == 2 else (23 + 2 * rad, 83 + 2 * rad, 141 + 2 * rad)
 
 
-def configs_for(an5d, st, ext, ndim):
+def configs_for(an5d, st, ext, ndim, direct=0):
     """A spread of available (bT, vec) configurations for this stencil, with short stream blocks so
     several stream blocks (and interior + edge launches) are exercised."""
     out = []
@@ -55,13 +55,13 @@ def configs_for(an5d, st, ext, ndim):
         bts = []
         for bT in range(1, 11):
             try:
-                st.describe(ext, {"bT": bT, "vec": vec, "h": 16})
+                st.describe(ext, {"bT": bT, "vec": vec, "h": 16, "direct": direct})
                 bts.append(bT)
             except an5d.AN5DError:
                 pass
         if bts:
             picks = sorted({bts[0], bts[len(bts) // 2], bts[-1]})
-            out += [{"bT": b, "vec": vec, "h": 16 if ndim == 2 else 8} for b in picks]
+            out += [{"bT": b, "vec": vec, "h": 16 if ndim == 2 else 8, "direct": direct} for b in picks]
     return out
 
 
@@ -118,6 +118,44 @@ def test_exact_integer_bit_identical(an5d, name, dtype):
         got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
         exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
         assert np.array_equal(got, exp), (name, cfg, T)
+
+
+@pytest.mark.parametrize("name", ["box2d1r", "box2d2r", "box2d3r", "box2d4r", "j2d9pt"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_direct_gather_variant(an5d, name, dtype):
+    """Partial sums OFF (Table 1 "Otherwise"; BASELINE config 4): the direct-gather
+    kernels match the oracle within tolerance on random inputs, bit-for-bit in exact-integer mode,
+    and store every interior cell exactly once."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    cfgs = configs_for(an5d, st, ext, ndim, direct=1)
+    assert cfgs, f"no direct instance for {name}"
+    tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    gx = inputs.global_grid(1234, ext, kind="pm")
+    for cfg in cfgs:
+        bT = cfg["bT"]
+        for T in sorted({1, bT, 2 * bT + 3}):
+            got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+            exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+            assert ring_equal(got, exp, rad), (cfg, T)
+            assert rel_linf(got, exp, rad) <= TOL[dtype], (name, cfg, T)
+        T = _exact_T(ndim, rad, shape, 2 * bT + 3, dtype)
+        if T >= 1:
+            got, _ = gpu_run(an5d, ndim, rad, shape, tabx, divx, gx, T, dtype, cfg)
+            assert np.array_equal(got, oracle.run(gx, rad, shape, tabx, divx, T, NP[dtype])), (name, cfg, T)
+        a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+        b = an5d.empty_grid(ext, rad, dtype)
+        wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+        st.copy_ring(a, b)
+        st.sweep(a, b, bT, cfg, write_count=wc)
+        torch.cuda.synchronize()
+        w = wc.cpu().numpy()
+        core = tuple(slice(rad, e - rad) for e in ext)
+        assert np.all(w[core] == 1), cfg
+        w[core] = 0
+        assert not w.any(), cfg
 
 
 @pytest.mark.parametrize("name", ["star2d1r", "box2d3r", "j2d9pt", "star3d2r", "box3d1r", "box3d4r"])
@@ -239,3 +277,28 @@ def test_slab_loopback_bit_identical(an5d, name, n_int, T, bT, nslab, dtype):
     full = ref.copy()
     full[rad:gext[0] - rad] = got
     assert rel_linf(full, exp, rad) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("name,dtype", [("star2d1r", torch.float32), ("box2d2r", torch.float64),
+                                        ("star3d1r", torch.float32)])
+def test_tune_then_run(an5d, name, dtype):
+    """an5d_tune (model top-k + measured pick) returns a feasible configuration that
+    honours the hint, leaves grid_in untouched, and the run with it matches the oracle."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, dtype)
+    a0 = a.clone()
+    cfg = st.tune(a, b, 7, {"h": 16}, top_k=3)
+    torch.cuda.synchronize()
+    assert cfg["h"] == 16 and cfg["bT"] >= 1 and cfg["seconds_per_cell_step"] > 0
+    assert torch.equal(a, a0)
+    cfg.pop("seconds_per_cell_step")
+    st.run(a, b, 7, cfg)
+    torch.cuda.synchronize()
+    exp = oracle.run(g, rad, shape, tab, div, 7, NP[dtype])
+    got = b.cpu().numpy()
+    assert ring_equal(got, exp, rad)
+    assert rel_linf(got, exp, rad) <= TOL[dtype]

@@ -148,3 +148,28 @@ def test_flops_per_cell_table2():
         assert perf.flops_per_cell(ndim, rad, shape, has_div) == g[name], name
     # eff_ALU for star2d1r: 4 FMA + 1 MUL -> 9/10
     assert abs(perf.eff_alu(2, 1, 0, False) - 0.9) < 1e-15
+
+
+def test_direct_variant_config(an5d):
+    """Partial sums off (config field `direct`, Table 1 "Otherwise" P:262-270): 2D box instances
+    exist and describe like the associative ones (same geometry formulas); 3D or an out-of-range
+    value is rejected before any launch."""
+    import torch
+
+    import inputs
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("box2d2r")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    ext = [16384 + 2 * rad] * 2
+    for bT in (1, 2, 3, 4):
+        g0 = st.describe(ext, {"bT": bT, "vec": 8, "h": 256})
+        g1 = st.describe(ext, {"bT": bT, "vec": 8, "h": 256, "direct": 1})
+        for k in ("bS", "compute", "halo_loaded", "n_tiles", "n_tb", "n_tb_prime", "stream_overlap"):
+            assert g0[k] == g1[k], k
+    with pytest.raises(an5d.AN5DError) as e:
+        st.describe(ext, {"bT": 2, "vec": 8, "h": 256, "direct": 2})
+    assert e.value.status == 1
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("box3d1r")
+    st3 = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    with pytest.raises(an5d.AN5DError) as e:
+        st3.describe([66, 66, 66], {"bT": 1, "vec": 2, "h": 32, "direct": 1})
+    assert e.value.status == 5
