@@ -251,7 +251,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
         if (qi < rlo || qi >= rhi) {                      // z-ring plane: every cell
 #pragma unroll
             for (int yy = 0; yy < VY; ++yy) load_row(u[yy], sq + yy * kTX);
-        } else if (EDGE && g.ring_xy) {                   // x/y-ring cells of this thread
+        } else if (EDGE && g.ring_xy && ring_mask) {      // x/y-ring cells of this thread
 #pragma unroll
             for (int yy = 0; yy < VY; ++yy) {
                 E o[NE];
@@ -292,6 +292,9 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 
     int i = 0;          // step counter since base0
     int slot_i = 0;     // i mod D
+    // element offset of this thread's patch in the plane the current step stores (advanced by one
+    // plane per step: no 64-bit multiplies in the store path)
+    int64_t st_off = (base0 - (int64_t)(BT - 1) * DL - R) * a.pz + (int64_t)gy0 * a.py + gx0;
     int xb = 0;         // exchange buffer parity
     const int64_t s_stop = g.s_end + (int64_t)(BT - 1) * SK;
     for (int64_t base = base0; base < s_stop; base += U) {
@@ -436,7 +439,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             if (pi >= rp0 && pi < rp1) {
                 const int64_t p = s - (int64_t)(BT - 1) * DL - R;
                 const auto& fin = acc[BT - 1][ROT ? 0 : pmod(k - (BT - 1) * DL - R, P)];
-                T* op = dst + p * a.pz + (int64_t)gy0 * a.py + gx0;
+                T* op = dst + st_off;
 #pragma unroll
                 for (int yy = 0; yy < VY; ++yy) {
                     T c[VX];
@@ -461,6 +464,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                     }
                 }
             }
+            st_off += a.pz;
             if constexpr (ROT) {
                 // slot j <- slot j+1: slot 0 (just completed and consumed) is recycled as the last
 #pragma unroll
