@@ -430,7 +430,7 @@ def run_an5d(args):
                    "vec": cfg["vec"], "h": cfg["h"], "partial_sums": "off" if cfg.get("direct") else "on",
                    "planner": "model" if args.no_tune else "model top-5, measured pick (P:784-793)",
                    "bS": geom["bS"][:nb], "bS_loaded": geom["bS_loaded"][:nb],
-                   "parallelism": "1 GPU", "l2": "inputs larger than L2 (1 GiB per grid buffer > 126 MB)",
+                   "parallelism": "1 GPU", "l2": f"inputs larger than L2 ({a.numel() * a.element_size() / 2**30:.2f} GiB per grid buffer > 126 MB)",
                    "regs_per_thread": geom["regs_per_thread"]},
         "gflops": round(gcells * F, 2),
         "roofline": rl,
