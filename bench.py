@@ -348,8 +348,11 @@ def run_an5d(args):
     clock_mhz = peaks.get("sm_max_mhz") or 1965.0
     fp_peak = perf.fp_peak_flops(elem, 148, clock_mhz)
     nb = ndim - 1
+    # 2D units are runs of stream blocks that pay the stream overlap once per run:
+    # the effective stream-block length is the tile-rows per unit
+    h_eff = geom["n_tiles"][0] * n / max(1, geom["n_units"]) if ndim == 2 else geom["h"]
     roof = perf.roofline(ndim=ndim, rad=rad, shape=shape, has_div=div != 1.0, dtype_bytes=elem, bT=cfg["bT"],
-                         tile_loaded=geom["bS_loaded"][:nb], tile_compute=geom["compute"][:nb], h=geom["h"],
+                         tile_loaded=geom["bS_loaded"][:nb], tile_compute=geom["compute"][:nb], h=h_eff,
                          hbm_gbs=peaks["hbm_gbs"], fp_peak=fp_peak)
 
     # ---- dominant kernel: one full-degree N.5D sweep (interior launch + concurrent edge launch),

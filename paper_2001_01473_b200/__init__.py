@@ -47,7 +47,7 @@ class Geometry(ctypes.Structure):
         ("n_tb", ctypes.c_int64), ("h", ctypes.c_int64), ("n_stream_blocks", ctypes.c_int64),
         ("n_tb_prime", ctypes.c_int64), ("stream_overlap", ctypes.c_int64), ("n_thr", ctypes.c_int),
         ("units_per_block", ctypes.c_int), ("grid_blocks", ctypes.c_int64), ("smem_bytes", ctypes.c_size_t),
-        ("regs_per_thread", ctypes.c_int), ("vec", ctypes.c_int),
+        ("regs_per_thread", ctypes.c_int), ("vec", ctypes.c_int), ("n_units", ctypes.c_int64),
     ]
 
     def as_dict(self):

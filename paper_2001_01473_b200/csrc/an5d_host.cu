@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -60,6 +61,8 @@ struct Plan {
     int64_t launches = 0;
     unsigned long long* ctr = nullptr;  // kCtrRing dynamic-scheduling counter pairs (device, zeroed)
     int64_t ctr_seq = 0;                // launches that used a counter pair
+    // 2D run tables (device, immutable once built), keyed by the sweep geometry they schedule
+    std::map<std::vector<int64_t>, std::pair<int4*, int64_t>> runs;
 };
 constexpr int kCtrRing = 64;            // counter pairs in flight per plan (>= concurrent sweeps)
 
@@ -251,6 +254,58 @@ int taps_of(const Plan& p) {
     return p.ndim == 2 ? 4 * p.rad + 1 : 6 * p.rad + 1;
 }
 
+// 2D unit schedule ("runs").  A persistent warp that streams k consecutive stream blocks of one
+// tile in a single pass pays the stream-block overlap (2 b_T rad rows) and the
+// pipeline prologue once instead of k times; the output rows and their values are identical
+// (every row is still produced by the same per-row arithmetic).  The table is handed out by the
+// kernel's dynamic counter in this order:
+//   1. x-edge tiles {0, nx-1, nx-2}: single stream blocks (slowest units first);
+//   2. y-edge stream blocks (those touching the ring / array end) of the other tiles: singles;
+//   3. one round of c = floor(W / n_interior_tiles) big runs per interior tile, k stream blocks
+//      each, covering about `frac` of the y-interior stream blocks (W = launched warps, so every
+//      warp gets about one big run);
+//   4. the remaining y-interior stream blocks as singles: the dynamic tail balances on these.
+// frac = AN5D_RUN_FRAC (default 0.85; 0 = singles only, the plain stream-block schedule).
+std::vector<int4> build_runs_2d(const SweepGeom& g, int64_t W, double frac) {
+    const int nx = (int)g.ntiles[0];
+    const int nxe = nx < 4 ? nx : 3, ni = nx - nxe;
+    std::vector<int4> r;
+    r.reserve((size_t)(nx * g.n_sb));
+    for (int64_t sb = 0; sb < g.n_sb; ++sb)
+        for (int e = 0; e < nxe; ++e) r.push_back(make_int4(nx < 4 ? e : (e == 0 ? 0 : nx - e), (int)sb, (int)sb + 1, 0));
+    if (ni == 0) return r;
+    // y-interior stream blocks: the interior rectangle's range when it exists, else none
+    int64_t lo = g.sb_lo, hi = g.sb_hi;
+    if (hi <= lo) lo = hi = g.n_sb;
+    for (int64_t sb = 0; sb < g.n_sb; ++sb)
+        if (sb < lo || sb >= hi)
+            for (int t = 1; t <= ni; ++t) r.push_back(make_int4(t, (int)sb, (int)sb + 1, 0));
+    const int64_t nI = hi - lo;
+    const int64_t c = std::max<int64_t>(1, W / ni);
+    const int64_t k = (int64_t)(frac * (double)nI / (double)c);
+    int64_t start = lo;
+    if (k >= 2) {
+        for (int64_t j = 0; j < c; ++j)
+            for (int t = 1; t <= ni; ++t) r.push_back(make_int4(t, (int)(lo + j * k), (int)(lo + (j + 1) * k), 0));
+        start = lo + c * k;
+    }
+    for (int64_t sb = start; sb < hi; ++sb)
+        for (int t = 1; t <= ni; ++t) r.push_back(make_int4(t, (int)sb, (int)sb + 1, 0));
+    return r;
+}
+
+double run_frac() {
+    const char* e = getenv("AN5D_RUN_FRAC");   // read per call: tests switch it within a process
+    return e ? std::max(0.0, std::min(0.98, atof(e))) : 0.85;
+}
+
+// warps the run table is shaped for: the launched persistent warps, or AN5D_RUN_WARPS (test knob:
+// forces long runs on grids small enough for the oracle)
+int64_t run_warps(int64_t blocks) {
+    const char* e = getenv("AN5D_RUN_WARPS");
+    return e && atoll(e) > 0 ? atoll(e) : blocks;
+}
+
 // Planner model: predicted seconds per cell-step of a configuration, in the
 // spirit of the paper's section 5 model (one time per resource, the max of them, a
 // waves efficiency) re-derived for this build's kernels on B200:
@@ -274,12 +329,19 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     int64_t cells_per_plane = 1;
     for (int i = 0; i < p.ndim - 1; ++i) cells_per_plane *= g.loaded[i];
     const double eta_hbm = 0.75, eta_fma = p.ndim == 2 ? 0.45 : 0.35;
-    const double bytes = (double)p.elem * ((double)g.n_units * rows_per_unit * cells_per_plane + (double)interior);
+    const double resident = (double)resident_blocks(inst) * di.n_sm;
+    // 2D: units are runs of stream blocks (build_runs_2d); each run pays the overlap once
+    double units = (double)g.n_units, unit_rows = (double)rows_per_unit;
+    if (p.ndim == 2 && run_frac() > 0) {
+        const double nt = (double)g.ntiles[0];
+        units = (double)build_runs_2d(g, std::min<int64_t>(g.n_units, (int64_t)resident), run_frac()).size();
+        unit_rows = nt * (double)(dm.E[0] - 2 * R) / units + 2.0 * bT * R;
+    }
+    const double bytes = (double)p.elem * (units * unit_rows * cells_per_plane + (double)interior);
     const double t_hbm = bytes / (di.hbm_gbs * 1e9 * eta_hbm);
-    const double fma_ops = (double)g.n_units * (rows_per_unit + 2 * R + 1) * cells_per_plane * bT * taps_of(p);
+    const double fma_ops = units * (unit_rows + 2 * R + 1) * cells_per_plane * bT * taps_of(p);
     const double lanes = p.dtype == AN5D_F64 ? 64.0 : 128.0;
     const double t_fma = fma_ops / (di.n_sm * lanes * di.clock_ghz * 1e9 * eta_fma);
-    const double resident = (double)resident_blocks(inst) * di.n_sm;
     const double tail = 1.0 + resident / std::max<double>(1.0, (double)g.n_units);
     const double t = std::max(t_hbm, t_fma) * tail;
     if (out_geom) *out_geom = g;
@@ -422,6 +484,8 @@ an5d_status ensure_streams(Plan& p) {
     if ((e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
     if ((e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
     if (p.ctr) cudaFree(p.ctr);
+    for (auto& kv : p.runs) cudaFree(kv.second.first);
+    p.runs.clear();
     if ((e = cudaMalloc(&p.ctr, sizeof(unsigned long long) * 2 * kCtrRing)) != cudaSuccess) return cuda_fail(e, "counter");
     if ((e = cudaMemset(p.ctr, 0, sizeof(unsigned long long) * 2 * kCtrRing)) != cudaSuccess) return cuda_fail(e, "counter");
     p.device = dev;
@@ -470,7 +534,6 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
     SweepGeom g{};
     an5d_status s = sweep_geometry(p, *inst, dm, d, cfg.h, g_off, gE0, out_lo, out_hi, g);
     if (s != AN5D_OK) return s;
-    const int64_t n_edge = g.n_units - g.n_interior;
     cudaError_t e;
     if (p.ndim == 2) {
         // one persistent launch over every (tile, stream block) unit, interior and edge alike
@@ -482,21 +545,37 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.wc = wc; a.Ex = (int)dm.E[1]; a.C = g.C[0]; a.H = g.halo[0]; a.n_tiles_x = (int)g.ntiles[0];
         const int64_t cap = (int64_t)resident_blocks(*inst) * dev_info().n_sm;
         const int64_t blocks = std::min<int64_t>(g.n_units, cap);
+        const double frac = run_frac();
+        if (frac > 0) {
+            const int64_t W = run_warps(blocks);
+            const std::vector<int64_t> key = {d, g.ntiles[0], g.n_sb, g.sb_lo, g.sb_hi, W, (int64_t)(frac * 1e6)};
+            auto it = p.runs.find(key);
+            if (it == p.runs.end()) {
+                const std::vector<int4> tab = build_runs_2d(g, W, frac);
+                int4* dtab = nullptr;
+                if ((e = cudaMalloc(&dtab, sizeof(int4) * tab.size())) != cudaSuccess) return cuda_fail(e, "run table");
+                if ((e = cudaMemcpy(dtab, tab.data(), sizeof(int4) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+                    return cuda_fail(e, "run table upload");
+                it = p.runs.emplace(key, std::make_pair(dtab, (int64_t)tab.size())).first;
+            }
+            a.runs = it->second.first;
+            a.n_units = it->second.second;
+        }
         // AN5D_UNIT_PROFILE=path: debug-only per-unit timing dump (synchronises; never in benches)
         const char* prof_path = getenv("AN5D_UNIT_PROFILE");
-        if (prof_path && !wc) cudaMalloc(&a.unit_ns, sizeof(long long) * 3 * g.n_units);
+        if (prof_path && !wc) cudaMalloc(&a.unit_ns, sizeof(long long) * 3 * a.n_units);
         if ((e = inst->launch2d(a, p.coeffs_dev_t.data(), blocks, false, st)) != cudaSuccess)
             return cuda_fail(e, "sweep launch");
         p.launches++;
         if (a.unit_ns) {
-            std::vector<long long> h(3 * g.n_units);
+            std::vector<long long> h(3 * a.n_units);
             cudaStreamSynchronize(st);
             cudaMemcpy(h.data(), a.unit_ns, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
             cudaFree(a.unit_ns);
             if (FILE* f = fopen(prof_path, "a")) {
-                fprintf(f, "# sweep degree %d n_units %lld ntx %lld h %lld blocks %lld\n", d, (long long)g.n_units,
+                fprintf(f, "# sweep degree %d n_units %lld ntx %lld h %lld blocks %lld\n", d, (long long)a.n_units,
                         (long long)g.ntiles[0], (long long)g.h, (long long)blocks);
-                for (int64_t u = 0; u < g.n_units; ++u)
+                for (int64_t u = 0; u < a.n_units; ++u)
                     fprintf(f, "%lld %lld %lld %lld\n", (long long)u, h[3 * u], h[3 * u + 1], h[3 * u + 2]);
                 fclose(f);
             }
@@ -660,6 +739,7 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
 an5d_status an5d_destroy(an5d_plan* p) {
     if (!p) return AN5D_OK;
     if (p->ctr) cudaFree(p->ctr);
+    for (auto& kv : p->runs) cudaFree(kv.second.first);
     if (p->side) {
         cudaStreamDestroy(p->side);
         cudaEventDestroy(p->ev_fork);
@@ -812,6 +892,9 @@ an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_confi
         out->grid_blocks = p->ndim == 2 ? std::min<int64_t>(g.n_units,
                                                             (int64_t)resident_blocks(*inst) * dev_info().n_sm)
                                         : g.n_units;
+        out->n_units = (p->ndim == 2 && run_frac() > 0)
+                           ? (int64_t)build_runs_2d(g, run_warps(out->grid_blocks), run_frac()).size()
+                           : g.n_units;
         out->smem_bytes = inst->smem_bytes;
         cudaFuncAttributes attr{};
         if (cudaFuncGetAttributes(&attr, inst->fn_interior) == cudaSuccess) out->regs_per_thread = attr.numRegs;

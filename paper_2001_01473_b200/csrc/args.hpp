@@ -21,6 +21,8 @@ struct Sweep2DArgs {
     int64_t n_sb;         // stream blocks
     int32_t* wc;          // debug: per-cell store counts (local Ey x Ex, dense), or nullptr
     long long* unit_ns;   // debug: per-unit (start, end, smid) globaltimer stamps, or nullptr
+    const int4* runs;     // unit -> {tile_x, first stream block, end stream block}, or nullptr
+                          // (then unit = one stream block in the fixed edge-first order)
     int Ex;               // x extent (ring included)
     int C;                // compute width per tile (aligned to 16 bytes)
     int H;                // loaded halo per side (>= degree*rad, multiple of the vector width)

@@ -302,3 +302,48 @@ def test_tune_then_run(an5d, name, dtype):
     got = b.cpu().numpy()
     assert ring_equal(got, exp, rad)
     assert rel_linf(got, exp, rad) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("name,dtype,cfg", [
+    ("star2d1r", torch.float32, {"bT": 3, "h": 8, "vec": 8}),
+    ("star2d1r", torch.float32, {"bT": 7, "h": 16, "vec": 8}),
+    ("box2d2r", torch.float64, {"bT": 2, "h": 8, "vec": 4}),
+    ("j2d5pt", torch.float32, {"bT": 4, "h": 8, "vec": 4}),
+])
+def test_stream_block_runs(an5d, name, dtype, cfg, monkeypatch):
+    """2D run schedule (an5d_host.cu build_runs_2d: x-edge singles, y-edge singles, one round of
+    long runs of consecutive stream blocks per interior tile, a tail of singles).  The run table is
+    shaped for 4 warps (AN5D_RUN_WARPS) so an oracle-sized grid gets runs of ~10-20 stream blocks:
+    result within tolerance of the oracle, bit-identical to the plain one-stream-block-per-unit
+    schedule (AN5D_RUN_FRAC=0: same per-row arithmetic), every interior cell stored exactly once."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = (203 + 2 * rad, 1100 + 2 * rad)   # >= 4 tiles across (interior tiles exist), ~25 stream blocks
+    g = inputs.global_grid(77, ext)
+    T = 2 * cfg["bT"] + 1
+    monkeypatch.setenv("AN5D_RUN_WARPS", "4")
+    got, st = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+    exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+    assert ring_equal(got, exp, rad)
+    assert rel_linf(got, exp, rad) <= TOL[dtype], (name, cfg)
+    monkeypatch.setenv("AN5D_RUN_FRAC", "0")
+    plain, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+    assert np.array_equal(got, plain), (name, cfg)
+    monkeypatch.delenv("AN5D_RUN_FRAC")
+    # exact-integer mode: bit-identical to the oracle
+    tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    gx = inputs.global_grid(1234, ext, kind="pm")
+    Tx = _exact_T(ndim, rad, shape, T, dtype)
+    gotx, _ = gpu_run(an5d, ndim, rad, shape, tabx, divx, gx, Tx, dtype, cfg)
+    assert np.array_equal(gotx, oracle.run(gx, rad, shape, tabx, divx, Tx, NP[dtype])), (name, cfg, Tx)
+    # one sweep with store counts (routes every unit through the EDGE loop, runs included)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, dtype)
+    wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+    st.copy_ring(a, b)
+    st.sweep(a, b, cfg["bT"], st.plan_config(ext, T, cfg), write_count=wc)
+    torch.cuda.synchronize()
+    w = wc.cpu().numpy()
+    core = tuple(slice(rad, e - rad) for e in ext)
+    assert np.all(w[core] == 1), cfg
+    w[core] = 0
+    assert not w.any(), cfg

@@ -173,3 +173,29 @@ def test_direct_variant_config(an5d):
     with pytest.raises(an5d.AN5DError) as e:
         st3.describe([66, 66, 66], {"bT": 1, "vec": 2, "h": 32, "direct": 1})
     assert e.value.status == 5
+
+
+def test_run_table_unit_count(an5d, monkeypatch):
+    """2D run schedule: with AN5D_RUN_FRAC=0 every unit is one stream block
+    (n_units == n_tb_prime); with runs, fewer units, never fewer than one per tile, and a
+    smaller table when it is shaped for fewer warps (longer runs).  3D is unaffected."""
+    import torch
+
+    import inputs
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("star2d1r")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    ext = [16384 + 2 * rad] * 2
+    cfg = {"bT": 4, "vec": 8, "h": 64}
+    monkeypatch.setenv("AN5D_RUN_FRAC", "0")
+    g0 = st.describe(ext, cfg)
+    assert g0["n_units"] == g0["n_tb_prime"]
+    monkeypatch.delenv("AN5D_RUN_FRAC")
+    g1 = st.describe(ext, cfg)
+    assert g0["n_tiles"][0] <= g1["n_units"] < g0["n_tb_prime"]
+    monkeypatch.setenv("AN5D_RUN_WARPS", "64")
+    g2 = st.describe(ext, cfg)
+    assert g0["n_tiles"][0] <= g2["n_units"] <= g1["n_units"]
+    monkeypatch.delenv("AN5D_RUN_WARPS")
+    s3 = an5d.Stencil(3, 1, shape, *inputs.coeff_table(3, 1, shape, seed=4), torch.float32)
+    g3 = s3.describe([514] * 3, {"bT": 2, "h": 64})
+    assert g3["n_units"] == g3["n_tb_prime"]
