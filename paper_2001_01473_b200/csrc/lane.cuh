@@ -56,33 +56,6 @@ template <int V> struct Lane<float, V> {
     __device__ static __forceinline__ float cell(const E (&P)[NE], int v) { return (v & 1) ? P[v >> 1].y : P[v >> 1].x; }
 };
 
-// fp32 "seam" layout of a lane's V = 2 x 4 cells: the lane holds the 16-byte vector at x = 4 lane
-// in each HALF of the 32 V-cell tile row, and element e pairs the cells e of the two halves,
-// (4 lane + e, 4 lane + e + 16 V).  Every x offset of a tap is then a whole element (the pair at
-// virtual position e + dx), so all taps are FFMA2 -- no scalar FFMAs for odd offsets; the in-row
-// halo is a pair from the neighbouring lane (the seam between the halves crosses lane 31 <-> 0).
-template <int V> struct LaneSeam {
-    using E = float2;
-    static constexpr int NE = V / 2;
-    static_assert(V == 8, "seam layout: two 16-byte vectors per lane");
-    __device__ static __forceinline__ E fma(E c, E q, E acc) { return __ffma2_rn(c, q, acc); }
-    __device__ static __forceinline__ E mul(E c, E q) { return __fmul2_rn(c, q); }
-    // cells in load order (vector 0 = first half, vector 1 = second half) <-> elements
-    __device__ static __forceinline__ void from_cells(E (&P)[NE], const float (&c)[V]) {
-#pragma unroll
-        for (int e = 0; e < NE; ++e) P[e] = make_float2(c[e], c[NE + e]);
-    }
-    __device__ static __forceinline__ void to_cells(float (&c)[V], const E (&P)[NE]) {
-#pragma unroll
-        for (int e = 0; e < NE; ++e) {
-            c[e] = P[e].x;
-            c[NE + e] = P[e].y;
-        }
-    }
-    __device__ static __forceinline__ float& cell(E (&P)[NE], int v) { return v < NE ? P[v].x : P[v - NE].y; }
-    __device__ static __forceinline__ float cell(const E (&P)[NE], int v) { return v < NE ? P[v].x : P[v - NE].y; }
-};
-
 // coefficient as an element (fp32: broadcast pair, pre-duplicated in the parameter table)
 template <typename T> struct CoefElem { using type = T; };
 template <> struct CoefElem<float> { using type = float2; };
