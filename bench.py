@@ -392,30 +392,62 @@ def run_an5d(args):
     rl["ideal_frac_step"] = round(gcells * 1e9 / roof["ideal_cells_s"], 4)
     rl["R_read"] = round(roof["R_read"], 4)
 
-    # ---- end to end through the public API with host buffers (pinned), copies inside the region
+    # ---- end to end through the public API with host buffers (pinned), copies inside the region.
+    # Every step copies its input grid host->device, runs T steps (an5d_run) and reads the result
+    # back.  Steps are pipelined over two device buffer pairs on three streams (H2D of step i+1 and
+    # D2H of step i-1 overlap the sweeps of step i; PCIe is full duplex) when the grids are small
+    # enough to double-buffer; otherwise serial on one stream.
     e2e = None
     if not args.no_e2e:
         stor = a.untyped_storage()
         nbytes = stor.nbytes()
-        host_in = torch.empty(nbytes // elem, dtype=dtype, pin_memory=True)
-        host_out = torch.empty_like(host_in)
-        host_in.copy_(torch.empty(0, dtype=dtype, device=dev).set_(a.untyped_storage()).cpu())
-        flat_a = torch.empty(0, dtype=dtype, device=dev).set_(a.untyped_storage())
-        flat_b = torch.empty(0, dtype=dtype, device=dev).set_(b.untyped_storage())
         k_e2e = max(2, min(args.steps, 5))
+        pipelined = nbytes <= (4 << 30)
+        nbuf = 2 if pipelined else 1
+        host_in = [torch.empty(nbytes // elem, dtype=dtype, pin_memory=True) for _ in range(nbuf)]
+        # (pinned explicitly: empty_like would return pageable memory, ~6 GB/s instead of ~50)
+        host_out = [torch.empty(nbytes // elem, dtype=dtype, pin_memory=True) for _ in range(nbuf)]
+        flat = lambda t: torch.empty(0, dtype=dtype, device=dev).set_(t.untyped_storage())
+        for h in host_in:
+            h.copy_(flat(a).cpu())
+        bufs = [(a, b)] + ([(an5d.empty_grid(ext, rad, dtype, dev), an5d.empty_grid(ext, rad, dtype, dev))]
+                           if pipelined else [])
+        s_in = torch.cuda.Stream(dev) if pipelined else stream
+        s_out = torch.cuda.Stream(dev) if pipelined else stream
+        ev_comp = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_in = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_out = [torch.cuda.Event() for _ in range(nbuf)]
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(k_e2e):
-            flat_a.copy_(host_in, non_blocking=True)
-            st.run(a, b, T, cfg)
-            host_out.copy_(flat_b, non_blocking=True)
+        s_in.wait_event(e0)
+        s_out.wait_event(e0)
+        for i in range(k_e2e):
+            j = i % nbuf
+            ga, gb = bufs[j]
+            if i >= nbuf:
+                s_in.wait_event(ev_comp[j])       # step i-2's sweeps no longer read buffer ga
+            with torch.cuda.stream(s_in):
+                flat(ga).copy_(host_in[j], non_blocking=True)
+            ev_in[j].record(s_in)
+            stream.wait_event(ev_in[j])
+            if i >= nbuf:
+                stream.wait_event(ev_out[j])      # step i-2's result has been read back from gb
+            st.run(ga, gb, T, cfg)
+            ev_comp[j].record(stream)
+            s_out.wait_event(ev_comp[j])
+            with torch.cuda.stream(s_out):
+                host_out[j].copy_(flat(gb), non_blocking=True)
+            ev_out[j].record(s_out)
+        for j in range(nbuf):
+            stream.wait_event(ev_out[j])
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / k_e2e
         e2e = {"value": round(cells * T / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GCells/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(e2e_ms, 3),
-               "steps": k_e2e}
+               "steps": k_e2e, "pipelined": pipelined}
+        del bufs
 
     cpu = None
     if not args.no_cpu_baseline:
