@@ -95,9 +95,10 @@ typedef struct {
     size_t smem_bytes;          /* dynamic shared memory per thread block                        */
     int regs_per_thread;        /* from cudaFuncGetAttributes of the instance (0 if unknown)     */
     int vec;                    /* register tiling factor V                                      */
-    int64_t n_units;            /* units one launch schedules: 3D = n_tb_prime; 2D = runs of the  */
-                                /* host run table (consecutive stream blocks of one tile streamed */
-                                /* in one pass, each paying stream_overlap once)   */
+    int64_t n_units;            /* units one launch schedules = entries of the host run table     */
+                                /* (consecutive stream blocks of one tile streamed in one pass,   */
+                                /* each paying stream_overlap once); n_tb_prime    */
+                                /* when AN5D_RUN_FRAC=0                                           */
 } an5d_geometry;
 
 /* Create a plan (Table 2).

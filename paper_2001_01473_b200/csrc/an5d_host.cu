@@ -294,6 +294,48 @@ std::vector<int4> build_runs_2d(const SweepGeom& g, int64_t W, double frac) {
     return r;
 }
 
+// 3D: the same schedule over (tile y, tile x) with the kernel's frame-first order: frame tiles (first
+// and last two in y and x: they may touch the ring and run the EDGE variant) as singles, z-edge
+// stream blocks of interior tiles as singles, one round of long runs per interior tile, the rest as
+// singles.  One thread block per entry, dispatched in index order by the hardware.
+std::vector<int4> build_runs_3d(const SweepGeom& g, int64_t W, double frac) {
+    const int ny = (int)g.ntiles[0], nx = (int)g.ntiles[1];
+    auto frame = [&](int ty, int tx) { return ny < 4 || nx < 4 || ty == 0 || ty >= ny - 2 || tx == 0 || tx >= nx - 2; };
+    std::vector<int4> r;
+    std::vector<std::pair<int, int>> inner;
+    for (int ty = 0; ty < ny; ++ty)
+        for (int tx = 0; tx < nx; ++tx)
+            if (!frame(ty, tx)) inner.emplace_back(ty, tx);
+    r.reserve((size_t)(ny * nx * g.n_sb));
+    for (int64_t sb = 0; sb < g.n_sb; ++sb)
+        for (int ty = 0; ty < ny; ++ty)
+            for (int tx = 0; tx < nx; ++tx)
+                if (frame(ty, tx)) r.push_back(make_int4(ty, tx, (int)sb, (int)sb + 1));
+    if (inner.empty()) return r;
+    int64_t lo = g.sb_lo, hi = g.sb_hi;
+    if (hi <= lo) lo = hi = g.n_sb;
+    for (int64_t sb = 0; sb < g.n_sb; ++sb)
+        if (sb < lo || sb >= hi)
+            for (auto& t : inner) r.push_back(make_int4(t.first, t.second, (int)sb, (int)sb + 1));
+    const int64_t ni = (int64_t)inner.size(), nI = hi - lo;
+    const int64_t c = std::max<int64_t>(1, W / ni);
+    const int64_t k = (int64_t)(frac * (double)nI / (double)c);
+    int64_t start = lo;
+    if (k >= 2) {
+        for (int64_t j = 0; j < c; ++j)
+            for (auto& t : inner) r.push_back(make_int4(t.first, t.second, (int)(lo + j * k), (int)(lo + (j + 1) * k)));
+        start = lo + c * k;
+    }
+    for (int64_t sb = start; sb < hi; ++sb)
+        for (auto& t : inner) r.push_back(make_int4(t.first, t.second, (int)sb, (int)sb + 1));
+    return r;
+}
+
+// run table of a sweep geometry for W resident blocks (2D: persistent warps; 3D: blocks)
+std::vector<int4> build_runs(int ndim, const SweepGeom& g, int64_t W, double frac) {
+    return ndim == 2 ? build_runs_2d(g, W, frac) : build_runs_3d(g, W, frac);
+}
+
 double run_frac() {
     const char* e = getenv("AN5D_RUN_FRAC");   // read per call: tests switch it within a process
     return e ? std::max(0.0, std::min(0.98, atof(e))) : 0.85;
@@ -330,11 +372,12 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     for (int i = 0; i < p.ndim - 1; ++i) cells_per_plane *= g.loaded[i];
     const double eta_hbm = 0.75, eta_fma = p.ndim == 2 ? 0.45 : 0.35;
     const double resident = (double)resident_blocks(inst) * di.n_sm;
-    // 2D: units are runs of stream blocks (build_runs_2d); each run pays the overlap once
+    // units are runs of stream blocks (build_runs_2d / _3d); each run pays the overlap once
     double units = (double)g.n_units, unit_rows = (double)rows_per_unit;
-    if (p.ndim == 2 && run_frac() > 0) {
-        const double nt = (double)g.ntiles[0];
-        units = (double)build_runs_2d(g, std::min<int64_t>(g.n_units, (int64_t)resident), run_frac()).size();
+    if (run_frac() > 0) {
+        const double nt = (double)g.ntiles[0] * (p.ndim == 3 ? (double)g.ntiles[1] : 1.0);
+        const int64_t W = p.ndim == 2 ? std::min<int64_t>(g.n_units, (int64_t)resident) : (int64_t)resident;
+        units = (double)build_runs(p.ndim, g, W, run_frac()).size();
         unit_rows = nt * (double)(dm.E[0] - 2 * R) / units + 2.0 * bT * R;
     }
     const double bytes = (double)p.elem * (units * unit_rows * cells_per_plane + (double)interior);
@@ -587,12 +630,29 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.src = src; a.dst = dst; a.pz = dm.pitch[0]; a.py = dm.pitch[1];
         a.Ez = dm.E[0]; a.g_off = g_off; a.gEz = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
         a.h = g.h; a.n_sb = g.n_sb; a.n_units = g.n_units; a.wc = wc;
+        const double frac = run_frac();
+        if (frac > 0) {
+            const int64_t W = run_warps((int64_t)resident_blocks(*inst) * dev_info().n_sm);
+            const std::vector<int64_t> key = {3, d, g.ntiles[0], g.ntiles[1], g.n_sb, g.sb_lo, g.sb_hi, W,
+                                              (int64_t)(frac * 1e6)};
+            auto it = p.runs.find(key);
+            if (it == p.runs.end()) {
+                const std::vector<int4> tab = build_runs_3d(g, W, frac);
+                int4* dtab = nullptr;
+                if ((e = cudaMalloc(&dtab, sizeof(int4) * tab.size())) != cudaSuccess) return cuda_fail(e, "run table");
+                if ((e = cudaMemcpy(dtab, tab.data(), sizeof(int4) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+                    return cuda_fail(e, "run table upload");
+                it = p.runs.emplace(key, std::make_pair(dtab, (int64_t)tab.size())).first;
+            }
+            a.runs = it->second.first;
+            a.n_units = it->second.second;
+        }
         a.Ey = (int)dm.E[1]; a.Ex = (int)dm.E[2];
         a.Cy = g.C[0]; a.Cx = g.C[1]; a.Hy = g.halo[0]; a.Hx = g.halo[1];
         a.nty = (int)g.ntiles[0]; a.ntx = (int)g.ntiles[1];
         CUtensorMap tm;
         if ((s = encode_tmap_3d(p, *inst, src, dm, tm, a.x_off)) != AN5D_OK) return s;
-        if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), tm, g.n_units, st)) != cudaSuccess)
+        if ((e = inst->launch3d(a, p.coeffs_dev_t.data(), tm, a.n_units, st)) != cudaSuccess)
             return cuda_fail(e, "sweep launch");
         p.launches++;
     }
@@ -892,9 +952,13 @@ an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_confi
         out->grid_blocks = p->ndim == 2 ? std::min<int64_t>(g.n_units,
                                                             (int64_t)resident_blocks(*inst) * dev_info().n_sm)
                                         : g.n_units;
-        out->n_units = (p->ndim == 2 && run_frac() > 0)
-                           ? (int64_t)build_runs_2d(g, run_warps(out->grid_blocks), run_frac()).size()
+        out->n_units = run_frac() > 0
+                           ? (int64_t)build_runs(p->ndim, g,
+                                                 run_warps(p->ndim == 2 ? out->grid_blocks
+                                                                        : (int64_t)resident_blocks(*inst) * dev_info().n_sm),
+                                                 run_frac()).size()
                            : g.n_units;
+        if (p->ndim == 3) out->grid_blocks = out->n_units;
         out->smem_bytes = inst->smem_bytes;
         cudaFuncAttributes attr{};
         if (cudaFuncGetAttributes(&attr, inst->fn_interior) == cudaSuccess) out->regs_per_thread = attr.numRegs;

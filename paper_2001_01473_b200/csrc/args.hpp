@@ -40,6 +40,8 @@ struct Sweep3DArgs {
     int64_t n_units;         // units of this sweep (= blocks)
     int64_t n_sb;            // stream blocks
     int32_t* wc;             // debug store counts (dense Ez x Ey x Ex) or nullptr
+    const int4* runs;        // unit -> {tile y, tile x, first stream block, end stream block}, or
+                             // nullptr (then unit = one stream block in the fixed frame-first order)
     int Ey, Ex;
     int Cy, Cx;              // compute region per tile
     int Hy, Hx;              // loaded halo per side (Hy = degree*rad; Hx rounded to 16 bytes)

@@ -508,8 +508,19 @@ an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf, const __grid_constant
     const int64_t unit = blockIdx.x;
     if (unit >= a.n_units) return;
     int ty, tx;
-    int64_t sb;
-    unit_to_tile3d(a, unit, ty, tx, sb);
+    int64_t sb, sb_end;
+    if (a.runs) {
+        // run table (host-built, launch_sweep): consecutive stream blocks [sb, sb_end) of one tile in
+        // one pass; blocks are dispatched in index order, so the table's order is the schedule
+        const int4 r = a.runs[unit];
+        ty = r.x;
+        tx = r.y;
+        sb = r.z;
+        sb_end = r.w;
+    } else {
+        unit_to_tile3d(a, unit, ty, tx, sb);
+        sb_end = sb + 1;
+    }
     Unit3D g;
     g.cy0 = R + ty * a.Cy;
     g.cy1 = min(g.cy0 + a.Cy, a.Ey - R);
@@ -518,7 +529,7 @@ an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf, const __grid_constant
     g.wy0 = g.cy0 - a.Hy;
     g.wx0 = g.cx0 - a.Hx;
     g.p0 = a.out_lo + sb * a.h;
-    g.p1 = min(g.p0 + a.h, a.out_hi);
+    g.p1 = min(a.out_lo + sb_end * a.h, a.out_hi);
     g.s_first = g.p0 - (int64_t)BT * R;
     g.s_end = g.p1 + (int64_t)BT * R;
     g.s_a = max(g.s_first, (int64_t)0);

@@ -347,3 +347,42 @@ def test_stream_block_runs(an5d, name, dtype, cfg, monkeypatch):
     assert np.all(w[core] == 1), cfg
     w[core] = 0
     assert not w.any(), cfg
+
+
+@pytest.mark.parametrize("name,dtype,cfg", [
+    ("star3d1r", torch.float32, {"bT": 3, "h": 4, "vec": 2}),
+    ("box3d1r", torch.float64, {"bT": 2, "h": 4, "vec": 2}),
+    ("star3d2r", torch.float32, {"bT": 2, "h": 4, "vec": 2}),
+])
+def test_stream_block_runs_3d(an5d, name, dtype, cfg, monkeypatch):
+    """3D run schedule (build_runs_3d): long runs forced by shaping the table for 2 blocks; oracle
+    parity, bit-identical to the plain schedule, exact-integer mode, store counts once."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = (41 + 2 * rad, 150 + 2 * rad, 290 + 2 * rad)   # >= 4 tiles in y and x (interior tiles), ~10 stream blocks
+    g = inputs.global_grid(78, ext)
+    T = 2 * cfg["bT"] + 1
+    monkeypatch.setenv("AN5D_RUN_WARPS", "2")
+    got, st = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+    exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+    assert ring_equal(got, exp, rad)
+    assert rel_linf(got, exp, rad) <= TOL[dtype], (name, cfg)
+    monkeypatch.setenv("AN5D_RUN_FRAC", "0")
+    plain, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+    assert np.array_equal(got, plain), (name, cfg)
+    monkeypatch.delenv("AN5D_RUN_FRAC")
+    tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    gx = inputs.global_grid(1234, ext, kind="pm")
+    Tx = _exact_T(ndim, rad, shape, T, dtype)
+    gotx, _ = gpu_run(an5d, ndim, rad, shape, tabx, divx, gx, Tx, dtype, cfg)
+    assert np.array_equal(gotx, oracle.run(gx, rad, shape, tabx, divx, Tx, NP[dtype])), (name, cfg, Tx)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, dtype)
+    wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+    st.copy_ring(a, b)
+    st.sweep(a, b, cfg["bT"], st.plan_config(ext, T, cfg), write_count=wc)
+    torch.cuda.synchronize()
+    w = wc.cpu().numpy()
+    core = tuple(slice(rad, e - rad) for e in ext)
+    assert np.all(w[core] == 1), cfg
+    w[core] = 0
+    assert not w.any(), cfg

@@ -178,7 +178,7 @@ def test_direct_variant_config(an5d):
 def test_run_table_unit_count(an5d, monkeypatch):
     """2D run schedule: with AN5D_RUN_FRAC=0 every unit is one stream block
     (n_units == n_tb_prime); with runs, fewer units, never fewer than one per tile, and a
-    smaller table when it is shaped for fewer warps (longer runs).  3D is unaffected."""
+    smaller table when it is shaped for fewer warps (longer runs); the same for 3D."""
     import torch
 
     import inputs
@@ -197,5 +197,8 @@ def test_run_table_unit_count(an5d, monkeypatch):
     assert g0["n_tiles"][0] <= g2["n_units"] <= g1["n_units"]
     monkeypatch.delenv("AN5D_RUN_WARPS")
     s3 = an5d.Stencil(3, 1, shape, *inputs.coeff_table(3, 1, shape, seed=4), torch.float32)
-    g3 = s3.describe([514] * 3, {"bT": 2, "h": 64})
-    assert g3["n_units"] == g3["n_tb_prime"]
+    g3 = s3.describe([514] * 3, {"bT": 2, "h": 16, "vec": 2})
+    assert g3["n_tb"] <= g3["n_units"] < g3["n_tb_prime"]
+    monkeypatch.setenv("AN5D_RUN_FRAC", "0")
+    g4 = s3.describe([514] * 3, {"bT": 2, "h": 16, "vec": 2})
+    assert g4["n_units"] == g4["n_tb_prime"] == g3["n_tb_prime"]
