@@ -65,6 +65,7 @@ struct Plan {
     std::map<std::vector<int64_t>, std::pair<int4*, int64_t>> runs;
 };
 constexpr int kCtrRing = 64;            // counter pairs in flight per plan (>= concurrent sweeps)
+constexpr size_t kRunCache = 64;        // run tables kept per plan
 
 }  // namespace an5d
 
@@ -593,6 +594,14 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
             const int64_t W = run_warps(blocks);
             const std::vector<int64_t> key = {d, g.ntiles[0], g.n_sb, g.sb_lo, g.sb_hi, W, (int64_t)(frac * 1e6)};
             auto it = p.runs.find(key);
+            if (it == p.runs.end() && p.runs.size() >= kRunCache) {
+                // bounded cache: a plan run over many geometries drops its tables (device-synchronous
+                // free; the stream order of earlier launches that read them is respected)
+                cudaDeviceSynchronize();
+                for (auto& kv : p.runs) cudaFree(kv.second.first);
+                p.runs.clear();
+                it = p.runs.end();
+            }
             if (it == p.runs.end()) {
                 const std::vector<int4> tab = build_runs_2d(g, W, frac);
                 int4* dtab = nullptr;
@@ -636,6 +645,14 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
             const std::vector<int64_t> key = {3, d, g.ntiles[0], g.ntiles[1], g.n_sb, g.sb_lo, g.sb_hi, W,
                                               (int64_t)(frac * 1e6)};
             auto it = p.runs.find(key);
+            if (it == p.runs.end() && p.runs.size() >= kRunCache) {
+                // bounded cache: a plan run over many geometries drops its tables (device-synchronous
+                // free; the stream order of earlier launches that read them is respected)
+                cudaDeviceSynchronize();
+                for (auto& kv : p.runs) cudaFree(kv.second.first);
+                p.runs.clear();
+                it = p.runs.end();
+            }
             if (it == p.runs.end()) {
                 const std::vector<int4> tab = build_runs_3d(g, W, frac);
                 int4* dtab = nullptr;
