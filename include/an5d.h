@@ -23,7 +23,15 @@
  *     Violations return AN5D_ERR_UNSUPPORTED before any launch (the Python binding allocates
  *     compliant views: paper_2001_01473_b200.empty_grid).
  *   - Pointers named grid_* are DEVICE pointers owned by the caller; the library retains none of
- *     them after a call returns and performs no hidden device allocation.
+ *     them after a call returns and never allocates grid-sized memory.  A plan owns small device
+ *     scheduling state: the dynamic-unit counters and the run tables of the geometries it has
+ *     swept (16 bytes per unit, at most 64 tables cached; uploaded synchronously on first use of a
+ *     geometry, so do not capture a geometry's first sweep in a CUDA graph); an5d_destroy frees it.
+ *   - Environment (tuning / test knobs, read per call): AN5D_RUN_FRAC (fraction of the y/z-
+ *     interior stream blocks scheduled as long runs, default 0.85, 0 = one stream block per unit),
+ *     AN5D_RUN_WARPS (resident blocks the run table is shaped for; tests), AN5D_FORCE_CFG
+ *     ("bT,vec,h" overrides the planner), AN5D_HBM_GBS (planner bandwidth), AN5D_UNIT_PROFILE
+ *     (debug per-unit timing dump; synchronises).
  *   - Streams: every launch goes to `cuda_stream` (a cudaStream_t; NULL = legacy default stream)
  *     and is asynchronous.  Argument/feasibility errors are detected before any launch, so an
  *     error return means nothing was written.  CUDA launch errors surface as AN5D_ERR_CUDA.
