@@ -307,34 +307,65 @@ def bench_main(args, workloads):
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    # end to end: host (pinned) slab in, owned planes out, every step, max over ranks
+    # end to end: host (pinned) slab in, owned planes out, every step, max over ranks.  Steps are
+    # pipelined over two slab buffer pairs (H2D of step i+1 and D2H of step i-1 overlap the sweeps
+    # and exchanges of step i) when a slab is small enough to double-buffer, else serial.
     e2e = None
     if not args.no_e2e:
         n_in = a.untyped_storage().nbytes() // a.element_size()
-        flat_a = torch.empty(0, dtype=dtype, device=dev).set_(a.untyped_storage())
-        host_in = torch.empty(n_in, dtype=dtype, pin_memory=True)
-        host_in.copy_(flat_a.cpu())
-        owned = _plane_view(b, s.out_lo, s.out_hi - s.out_lo)
-        host_out = torch.empty(owned.numel(), dtype=dtype, pin_memory=True)
+        flat = lambda t: torch.empty(0, dtype=dtype, device=dev).set_(t.untyped_storage())
+        pipelined = a.untyped_storage().nbytes() <= (4 << 30)
+        nbuf = 2 if pipelined else 1
+        pairs = [(a, b)] + ([(an5d.empty_grid(lext, rad, dtype, dev), an5d.empty_grid(lext, rad, dtype, dev))]
+                            if pipelined else [])
+        host_in = [torch.empty(n_in, dtype=dtype, pin_memory=True) for _ in range(nbuf)]
+        for h_ in host_in:
+            h_.copy_(flat(a).cpu())
+        owned = [_plane_view(pb, s.out_lo, s.out_hi - s.out_lo) for _, pb in pairs]
+        host_out = [torch.empty(owned[0].numel(), dtype=dtype, pin_memory=True) for _ in range(nbuf)]
+        main = torch.cuda.current_stream(dev)
+        s_in = torch.cuda.Stream(dev) if pipelined else main
+        s_out = torch.cuda.Stream(dev) if pipelined else main
+        ev_in = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_comp = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_out = [torch.cuda.Event() for _ in range(nbuf)]
         k_e2e = max(2, min(args.steps, 5))
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(k_e2e):
-            flat_a.copy_(host_in, non_blocking=True)
-            run_distributed(st, s, (a, b), T, cfg, comm_stream=comm)
-            host_out.copy_(owned, non_blocking=True)
-        e1.record()
+        e0.record(main)
+        s_in.wait_event(e0)
+        s_out.wait_event(e0)
+        for i in range(k_e2e):
+            j = i % nbuf
+            ga, gb = pairs[j]
+            if i >= nbuf:
+                s_in.wait_event(ev_comp[j])
+            with torch.cuda.stream(s_in):
+                flat(ga).copy_(host_in[j], non_blocking=True)
+            ev_in[j].record(s_in)
+            main.wait_event(ev_in[j])
+            if i >= nbuf:
+                main.wait_event(ev_out[j])
+            run_distributed(st, s, (ga, gb), T, cfg, comm_stream=comm)
+            ev_comp[j].record(main)
+            s_out.wait_event(ev_comp[j])
+            with torch.cuda.stream(s_out):
+                host_out[j].copy_(owned[j], non_blocking=True)
+            ev_out[j].record(s_out)
+        for j in range(nbuf):
+            main.wait_event(ev_out[j])
+        e1.record(main)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        nb = torch.tensor([float(host_in.numel() * host_in.element_size()),
-                           float(host_out.numel() * host_out.element_size())], dtype=torch.float64, device=dev)
+        nb = torch.tensor([float(n_in * a.element_size()), float(host_out[0].numel() * a.element_size())],
+                          dtype=torch.float64, device=dev)
         dist.all_reduce(nb)
         e2e = {"value": round(float(n) ** ndim * T / (float(te.item()) * 1e-3) / 1e9, 3), "unit": "GCells/s",
                "h2d_bytes_per_step": int(nb[0].item()), "d2h_bytes_per_step": int(nb[1].item()),
-               "ms_per_step": round(float(te.item()), 3), "steps": k_e2e}
+               "ms_per_step": round(float(te.item()), 3), "steps": k_e2e, "pipelined": pipelined}
+        del pairs
     cells = float(n) ** ndim
     gcells = cells * T / (ms * 1e-3) / 1e9
     F = perf.flops_per_cell(ndim, rad, shape, div != 1.0)
