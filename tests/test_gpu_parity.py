@@ -386,3 +386,69 @@ def test_stream_block_runs_3d(an5d, name, dtype, cfg, monkeypatch):
     assert np.all(w[core] == 1), cfg
     w[core] = 0
     assert not w.any(), cfg
+
+
+def _bench_cfg(st, a, b, T):
+    """The launch configuration bench.py times: the measured top-5 pick (an5d_tune)."""
+    cfg = st.tune(a, b, T, None, top_k=5)
+    cfg.pop("seconds_per_cell_step", None)
+    return cfg
+
+
+def test_full_size_default_workload_sampled(an5d):
+    """BASELINE config 2's bench workload at full size and full T (star2d1r fp32, 16384^2, T=1000)
+    in bench.py's tuned configuration, checked on sampled outputs: the oracle runs on the window of
+    radius T*rad + rad around each sample (clipped to the array; a cropped frame cannot reach the
+    sample in T steps, and where the window is clipped its frame is the true ring), so each sampled
+    value is the oracle's exact full-grid value.  Samples: near a corner, on an edge, the centre,
+    and a cell at a tile / stream-block seam of the chosen configuration."""
+    name, n, T = "star2d1r", 16384, 1000
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = (n + 2 * rad,) * 2
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext).astype(np.float32)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    a = an5d.to_grid(torch.from_numpy(g).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, torch.float32)
+    cfg = _bench_cfg(st, a, b, T)
+    a = an5d.to_grid(torch.from_numpy(g).cuda(), rad)   # tune overwrote b only; rebuild a anyway
+    st.run(a, b, T, cfg)
+    torch.cuda.synchronize()
+    geo = st.describe(ext, cfg)
+    seam_x = rad + geo["compute"][0] * 3 - 1                 # last cell of tile 2
+    seam_y = rad + cfg["h"] * 5                              # first row of stream block 5
+    M = T * rad + rad
+    for (py, px) in [(rad + 3, rad + 5), (rad, n // 2 + 7), (n // 2, n // 2 + 1), (seam_y, seam_x)]:
+        y0, y1 = max(0, py - M), min(ext[0], py + M + 1)
+        x0, x1 = max(0, px - M), min(ext[1], px + M + 1)
+        win = np.ascontiguousarray(g[y0:y1, x0:x1])
+        exp = oracle.run(win, rad, shape, tab, div, T, np.float32)[py - y0, px - x0]
+        got = float(b[py, px].item())
+        assert abs(got - exp) <= 1e-5 * max(abs(exp), 1e-30), ((py, px), got, exp, cfg)
+
+
+@pytest.mark.parametrize("name", ["star2d1r", "star2d4r", "box2d2r", "star3d2r", "box3d1r"])
+def test_full_size_linear_field_exact(an5d, name):
+    """Full BASELINE size and T = 1000 in bench.py's tuned configuration (fp64): a symmetric stencil
+    with sum 1 maps a linear field to itself (oracle pin `test_linear_field_fixed_point`), and with
+    dyadic coefficients and a dyadic field every product and partial sum is exact in fp64 -- so the
+    result must equal the input bit-for-bit in EVERY cell.  A wrong tap offset, halo, tile seam,
+    stream-block seam, ring mask or run boundary anywhere in the 16384^2 / 512^3 grid breaks it."""
+    ndim, rad, shape, _, _ = inputs.benchmark_problem(name)
+    tab, div = inputs.coeff_table(ndim, rad, shape, seed=5, symmetric=True)
+    n = 16384 if ndim == 2 else 512
+    ext = (n + 2 * rad,) * ndim
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float64)
+    a = an5d.empty_grid(ext, rad, torch.float64)
+    b = an5d.empty_grid(ext, rad, torch.float64)
+    idx = [torch.arange(e, dtype=torch.float64, device="cuda") for e in ext]
+    if ndim == 2:
+        lin = 1.0 + (2 * idx[0][:, None] + idx[1][None, :]) * 2.0 ** -15
+    else:
+        lin = 1.0 + (3 * idx[0][:, None, None] + 2 * idx[1][None, :, None] + idx[2][None, None, :]) * 2.0 ** -12
+    a.copy_(lin)
+    cfg = _bench_cfg(st, a, b, 1000)
+    a.copy_(lin)
+    b.fill_(float("nan"))   # every cell of the result must be written by this run
+    st.run(a, b, 1000, cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(b, lin), (name, cfg, float((b - lin).abs().max()))
