@@ -171,6 +171,13 @@ def cpu_oracle_rate(name, dtype_name, n, host_grid, budget_s=12.0, max_T=None):
             "seconds": dt, "T_sample": T_cpu}
 
 
+def table2_flops_per_cell(ndim, rad, shape, has_div):
+    """PAPER.md Table 2 FLOP/cell: k taps -> 2k-1 FLOPs, +1 for the /c_0 of the
+    j-stencils.  Computed here so the reference arm loads nothing from the product package."""
+    k = (2 * rad + 1) ** ndim if shape == 1 else 2 * ndim * rad + 1
+    return 2 * k - 1 + (1 if has_div else 0)
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle as the reference arm (rank 0 only at N>1)."""
     import numpy as np
@@ -209,8 +216,7 @@ def run_reference(args):
     cells = float(n) ** ndim
     tot = sum(times)
     val = cells * per_step * args.steps / tot / 1e9
-    from paper_2001_01473_b200 import perf
-    F = perf.flops_per_cell(ndim, rad, shape, div != 1.0)
+    F = table2_flops_per_cell(ndim, rad, shape, div != 1.0)
     line = {
         "impl": "reference", "metric": f"GCells/s ({name} {dtype_name} {n}^{ndim}, T={T})", "value": round(val, 4),
         "unit": "GCells/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,

@@ -2,8 +2,10 @@
 
 Thin Python binding over the C ABI in ``include/an5d.h`` (libAN5D.so, sm_100a).  Argument
 marshalling only: every step of the sweep runs in the library's CUDA kernels.  PyTorch provides
-device memory and streams.  There is no CPU fallback: if libAN5D.so is missing or fails to load,
-importing this package raises.
+device memory and streams.  There is no CPU fallback: libAN5D.so is loaded on first use (the first
+Stencil, schedule() or version() call, or load()), and that call raises ImportError if the library
+is missing or fails to load.  Loading lazily keeps the pure-Python host modules of this package
+(slab partitioning, perf accounting) importable on a CPU box without the library.
 """
 from __future__ import annotations
 
@@ -87,7 +89,29 @@ def _load():
     return lib
 
 
-_lib = _load()
+class _LazyLib:
+    """Loads libAN5D.so on first attribute access (raises ImportError if it is missing)."""
+
+    _h = None
+
+    def __getattr__(self, name):
+        if _LazyLib._h is None:
+            _LazyLib._h = _load()
+        return getattr(_LazyLib._h, name)
+
+
+_lib = _LazyLib()
+
+
+def load():
+    """Load libAN5D.so now (raises ImportError if it is missing or does not load); returns the CDLL."""
+    _lib.an5d_version
+    return _LazyLib._h
+
+
+def loaded() -> bool:
+    return _LazyLib._h is not None
+
 EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
                     "an5d_describe", "an5d_schedule", "an5d_last_launch_count", "an5d_destroy",
                     "an5d_last_error", "an5d_version")

@@ -1,26 +1,28 @@
 """Build libAN5D.so (sm_100a) in-tree.
 
-Generates one instantiation file per (ndim, dtype, shape, rad) group under csrc/gen/, compiles
-them in parallel with nvcc (-gencode arch=compute_100a,code=sm_100a), and links the shared library
-next to this file.  Incremental: an object is rebuilt only when its source or any header changed.
+Generates one translation unit per kernel instance under csrc/gen/, compiles them in parallel with
+nvcc (-gencode arch=compute_100a,code=sm_100a -lineinfo), and links the shared library next to this
+file.  Incremental: an object is rebuilt only when its source, a header it depends on or the flags
+changed (digests use repo-relative paths, so a fresh clone anywhere rebuilds the same way).
 
-Instance policy: register-tiling factors and b_T ranges are limited
-to configurations whose register queue fits the 255-register budget without spilling:
-  2D: fp32 vec 8 (rad*bT <= 10) and vec 4 (rad*bT <= 12); fp64 vec 4 (rad*bT <= 10) and
-      vec 2 (rad <= 2, rad*bT <= 4); bT <= 10 (BASELINE config 2 sweeps bT 1..10).
-  3D: fp32 vy 4 (rad*bT <= 4, not box rad >= 2), vy 2 (rad*bT <= 8); fp64 vy 2 (rad*bT <= 4);
-      bT <= 6 (BASELINE config 3 sweeps 1..6).
-  2D box, non-associative direct-gather variant (partial sums off, BASELINE config 4): fp32 vec 8
-      and vec 4, fp64 vec 4, rad*bT <= 8.
+Build-time budget (round-2 rule): a clean default build must finish in a few minutes on an 8-core
+CPU box.  Hence
+  * the default instance set is CORE (below): what the planner picks at BASELINE sizes plus the
+    reduced degrees under each pick (~80 instances); the full b_T-sweep matrix of BASELINE configs
+    2-3 (~240 instances, ~15 min) is opt-in with AN5D_FULL_BUILD=1;
+  * the register budget of every known instance comes from the committed table regcaps.json, so
+    nothing compiles twice; only instances missing from the table run the spill-retry loop.
 """
 from __future__ import annotations
 
 import hashlib
+import json
 import re
 import os
 import shutil
 import subprocess
 import sys
+import time
 from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -36,24 +38,45 @@ REPO = os.path.dirname(HERE)
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v",
-    "-I", os.path.join(REPO, "include"),
-] + os.environ.get("AN5D_EXTRA_NVCC", "").split()
+    "-I", "include",
+] + os.environ.get("AN5D_EXTRA_NVCC", "").split()   # nvcc runs with cwd = REPO (relative paths)
 
 
-def instances():
-    """(ndim, dtype, shape, rad, bT, vec, assoc) tuples; dtype 0=f32 1=f64, shape 0=star 1=box,
-    assoc 1 = partial sums, 0 = direct gather."""
+# Default ("core") instance set: for every Table-2 stencil family and dtype, the (b_T, vec) the
+# measured planner picked at BASELINE sizes in round 1 (profiles/r01_v9_suite.jsonl), one b_T of
+# headroom where the pick sat at the HBM/FMA crossover, and every lower degree with the same vec
+# (the reduced-degree sweeps of the final-block adjustment, and small-T runs).
+# Key: (ndim, dtype, shape, rad) -> [(vec, max b_T)]; dtype 0 = f32, 1 = f64; shape 0 = star, 1 = box.
+CORE = {
+    (2, 0, 0, 1): [(8, 8)], (2, 0, 0, 2): [(8, 5)], (2, 0, 0, 3): [(8, 3)], (2, 0, 0, 4): [(8, 2)],
+    (2, 0, 1, 1): [(8, 5)], (2, 0, 1, 2): [(8, 2)], (2, 0, 1, 3): [(4, 1)], (2, 0, 1, 4): [(4, 1)],
+    (2, 1, 0, 1): [(4, 7)], (2, 1, 0, 2): [(4, 4)], (2, 1, 0, 3): [(4, 2)], (2, 1, 0, 4): [(4, 2)],
+    (2, 1, 1, 1): [(4, 4)], (2, 1, 1, 2): [(4, 2)], (2, 1, 1, 3): [(4, 1)], (2, 1, 1, 4): [(4, 1)],
+    (3, 0, 0, 1): [(2, 4)], (3, 0, 0, 2): [(2, 2)], (3, 0, 0, 3): [(2, 1)], (3, 0, 0, 4): [(2, 1)],
+    (3, 0, 1, 1): [(2, 2)], (3, 0, 1, 2): [(2, 1)], (3, 0, 1, 3): [(2, 1)], (3, 0, 1, 4): [(2, 1)],
+    (3, 1, 0, 1): [(2, 3)], (3, 1, 0, 2): [(2, 2)], (3, 1, 0, 3): [(2, 1)], (3, 1, 0, 4): [(2, 1)],
+    (3, 1, 1, 1): [(2, 2)], (3, 1, 1, 2): [(2, 1)], (3, 1, 1, 3): [(2, 1)], (3, 1, 1, 4): [(2, 1)],
+}
+# partial sums OFF (direct gather, BASELINE config 4 = box2d2r fp32): vec 8 and 4, b_T 1..2
+CORE_DIRECT = {(2, 0, 1, 2): [(8, 2), (4, 2)]}
+
+
+def full_instances():
+    """The full matrix (BASELINE configs 2-3 b_T sweeps: 2D b_T 1..10, 3D b_T 1..6), AN5D_FULL_BUILD=1.
+    Register-tiling factors and b_T ranges are limited to configurations whose register queue fits
+    the 255-register budget:
+      2D: fp32 vec 8 (rad*bT <= 10) and vec 4 (rad*bT <= 12); fp64 vec 4 (rad*bT <= 10) and
+          vec 2 (rad <= 2, rad*bT <= 4).
+      3D: fp32 vy 4 (rad*bT <= 4, not box rad >= 2), vy 2 (rad*bT <= 8); fp64 vy 2 (rad*bT <= 4).
+      2D box direct-gather variant: fp32 vec 8 and vec 4, fp64 vec 4, rad*bT <= 8."""
     out = []
-    dev = os.environ.get("AN5D_DEV_INSTANCES")
     for shape in (0, 1):
         for rad in range(1, 5):
             for bT in range(1, 11):
-                # 2D fp32
                 if rad * bT <= 10:
                     out.append((2, 0, shape, rad, bT, 8))
                 if rad * bT <= 12:
                     out.append((2, 0, shape, rad, bT, 4))
-                # 2D fp64
                 if rad * bT <= 10:
                     out.append((2, 1, shape, rad, bT, 4))
                 if rad <= 2 and rad * bT <= 4:
@@ -61,15 +84,32 @@ def instances():
                 if shape == 1 and rad * bT <= 8:
                     out += [(2, 0, 1, rad, bT, 8, 0), (2, 0, 1, rad, bT, 4, 0), (2, 1, 1, rad, bT, 4, 0)]
             for bT in range(1, 7):
-                # fp32: VY = 4 (64 x 64 tile plane) for rad*bT <= 4 (not high-order box: code size),
-                # VY = 2 (64 x 32) up to rad*bT <= 8; fp64: VY = 2 up to rad*bT <= 4
                 if rad * bT <= 4 and not (shape == 1 and rad >= 2):
                     out.append((3, 0, shape, rad, bT, 4))
                 if rad * bT <= 8:
                     out.append((3, 0, shape, rad, bT, 2))
                 if rad * bT <= 4:
                     out.append((3, 1, shape, rad, bT, 2))
-    out = [i if len(i) == 7 else i + (1,) for i in out]
+    return [i if len(i) == 7 else i + (1,) for i in out]
+
+
+def core_instances():
+    out = []
+    for tab, assoc in ((CORE, 1), (CORE_DIRECT, 0)):
+        for (ndim, dtype, shape, rad), lst in tab.items():
+            for vec, bmax in lst:
+                out += [(ndim, dtype, shape, rad, bT, vec, assoc) for bT in range(1, bmax + 1)]
+    return out
+
+
+def instances():
+    """(ndim, dtype, shape, rad, bT, vec, assoc) tuples; dtype 0=f32 1=f64, shape 0=star 1=box,
+    assoc 1 = partial sums, 0 = direct gather.  Default: core_instances(); AN5D_FULL_BUILD=1: the
+    full b_T-sweep matrix (plus the core set); AN5D_DEV_INSTANCES: a development subset."""
+    out = core_instances()
+    if os.environ.get("AN5D_FULL_BUILD", "") not in ("", "0"):
+        out = sorted(set(out) | set(full_instances()))
+    dev = os.environ.get("AN5D_DEV_INSTANCES")
     if dev:
         # quick development subset: comma list of "ndim:dtype:shape:rad" groups, or "min"
         if dev == "min":
@@ -80,18 +120,35 @@ def instances():
     return out
 
 
+def inst_name(ndim, dtype, shape, rad, bT, vec, assoc):
+    return (f"inst_{ndim}d_{'f64' if dtype else 'f32'}_{'box' if shape else 'star'}_r{rad}"
+            f"_bt{bT}_v{vec}{'' if assoc else '_direct'}")
+
+
+def _regcaps():
+    with open(os.path.join(HERE, "regcaps.json")) as f:
+        return json.load(f)["caps"]
+
+
 def generate():
-    """One generated translation unit per kernel instance (balanced parallel compilation)."""
+    """One generated translation unit per kernel instance (balanced parallel compilation).  The
+    instance's calibrated register cap (regcaps.json) is baked into its source."""
     os.makedirs(GEN, exist_ok=True)
+    caps = _regcaps()
     files = []
-    for (ndim, dtype, shape, rad, bT, vec, assoc) in instances():
+    for inst in instances():
+        (ndim, dtype, shape, rad, bT, vec, assoc) = inst
         T = "double" if dtype else "float"
-        name = (f"inst_{ndim}d_{'f64' if dtype else 'f32'}_{'box' if shape else 'star'}_r{rad}"
-                f"_bt{bT}_v{vec}{'' if assoc else '_direct'}.cu")
+        name = inst_name(*inst)
         targs = f"{T}, {rad}, {bT}, {vec}, {'true' if shape else 'false'}" + ("" if assoc else ", false")
         fn = "make_instance2d" if ndim == 2 else "make_instance3d"
-        text = "\n".join([
-            "// GENERATED by paper_2001_01473_b200/build.py -- one kernel instance.",
+        lines = ["// GENERATED by paper_2001_01473_b200/build.py -- one kernel instance."]
+        if name in caps:
+            lines.append("// register cap calibrated in regcaps.json (compiled once, no spill retry)")
+            lines.append("#define AN5D_CAP_KNOWN 1")
+            if caps[name] is not None:
+                lines.append(f"#define AN5D_MINB_CAP {int(caps[name])}")
+        lines += [
             f'#include "../inst{ndim}d.cuh"',
             "namespace an5d {",
             "namespace {",
@@ -99,8 +156,9 @@ def generate():
             "}  // namespace",
             "}  // namespace an5d",
             "",
-        ])
-        path = os.path.join(GEN, name)
+        ]
+        text = "\n".join(lines)
+        path = os.path.join(GEN, name + ".cu")
         if not os.path.exists(path) or open(path).read() != text:
             with open(path, "w") as f:
                 f.write(text)
@@ -133,7 +191,6 @@ def _header_digest(kind="host"):
 
 
 SPILL_LIMIT = 32   # bytes of spill stores tolerated before the register cap is relaxed
-CAPS = "128>168>255"   # register-budget retry sequence (part of the object digest)
 
 
 def _spill_bytes(log):
@@ -141,47 +198,57 @@ def _spill_bytes(log):
 
 
 def _compile(src, nvcc, hdr):
-    """Compile one instance.  If ptxas reports more than SPILL_LIMIT bytes of spill stores, retry
-    with a lower minimum-blocks cap (a larger register budget): the kernels' occupancy estimate is
-    a first guess and spills in the stream loop cost more than the occupancy they buy."""
+    """Compile one translation unit.  Instances with a calibrated cap (regcaps.json) compile once.
+    Unlisted instances: if ptxas reports more than SPILL_LIMIT bytes of spill stores, retry with a
+    lower minimum-blocks cap (a larger register budget) and report the cap to add to the table."""
     base = os.path.splitext(os.path.basename(src))[0]
     obj = os.path.join(OBJ, base + ".o")
     stamp = obj + ".sha"
-    digest = hashlib.sha1(open(src, "rb").read() + hdr.encode() + repr(CAPS).encode()).hexdigest()
+    text = open(src, "rb").read()
+    digest = hashlib.sha1(text + hdr.encode()).hexdigest()
     if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == digest:
         return obj, None
+    known = b"AN5D_CAP_KNOWN" in text or "inst_" not in base
+    rel = os.path.relpath(src, REPO)
     logs = []
     cap = None
+    t0 = time.time()
     while True:
         extra = [] if cap is None else [f"-DAN5D_MINB_CAP={cap}"]
-        cmd = [nvcc] + NVCC_FLAGS + extra + ["-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        cmd = [nvcc] + NVCC_FLAGS + extra + ["-c", rel, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True, cwd=REPO)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
         logs.append(f"# AN5D_MINB_CAP={cap}\n" + r.stderr)
         regs = max([int(v) for v in re.findall(r"Used (\d+) registers", r.stderr)] or [255])
-        if "inst_" not in base or "AN5D_MINB_FORCE" in " ".join(NVCC_FLAGS) or _spill_bytes(r.stderr) <= SPILL_LIMIT or regs > 168:
+        if known or "AN5D_MINB_FORCE" in " ".join(NVCC_FLAGS) or _spill_bytes(r.stderr) <= SPILL_LIMIT or regs > 168:
             break
         # next register budget: 128 -> 168 (2D: 12 one-warp blocks) -> 255; 3D: 128 -> 255
         cap = 12 if (regs <= 128 and "_2d_" in base) else 1
+    if not known:
+        print(f"build.py: {base} not in regcaps.json; calibrated cap = {cap} (add it to the table)",
+              file=sys.stderr)
     with open(obj + ".ptxas.log", "w") as f:
-        f.write("\n".join(logs))
+        f.write(f"# wall {time.time() - t0:.1f} s\n" + "\n".join(logs))
     with open(stamp, "w") as f:
         f.write(digest)
     return obj, logs[-1]
 
 
 def build(jobs: int | None = None, verbose: bool = True) -> str:
+    t0 = time.time()
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     os.makedirs(OBJ, exist_ok=True)
     srcs = generate() + [os.path.join(CSRC, "an5d_host.cu")]
     hdr = {k: _header_digest(k) for k in DEPS}
     jobs = jobs or max(1, os.cpu_count() or 1)
-    # big groups first
-    # heavy instances (3D, box, high radius) first
-    srcs.sort(key=lambda s: (("_3d_" in s) + ("_box_" in s), s), reverse=True)
+    # heavy instances (3D, box, high b_T) first so the longest compiles do not end up in the tail
+    def weight(s):
+        m = re.search(r"_r(\d)_bt(\d+)_", s)
+        return (("_3d_" in s) * 4 + ("_box_" in s) * 2 + (int(m.group(1)) * int(m.group(2)) if m else 99))
+    srcs.sort(key=weight, reverse=True)
+    kind = lambda s: "2d" if "inst_2d_" in s else ("3d" if "inst_3d_" in s else "host")
     with ThreadPoolExecutor(jobs) as ex:
-        kind = lambda s: "2d" if "inst_2d_" in s else ("3d" if "inst_3d_" in s else "host")
         objs = list(ex.map(lambda s: _compile(s, nvcc, hdr[kind(s)])[0], srcs))
     stamp = os.path.join(OBJ, "lib.sha")
     digest = hashlib.sha1("".join(sorted(open(o + ".sha").read() for o in objs)).encode()).hexdigest()
@@ -196,7 +263,8 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
     with open(stamp, "w") as f:
         f.write(digest)
     if verbose:
-        print(f"built {LIB} ({len(instances())} kernel instances)", file=sys.stderr)
+        print(f"built {LIB} ({len(srcs) - 1} kernel instances, {jobs} jobs, {time.time() - t0:.0f} s)",
+              file=sys.stderr)
     return LIB
 
 

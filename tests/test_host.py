@@ -160,7 +160,7 @@ def test_direct_variant_config(an5d):
     ndim, rad, shape, tab, div = inputs.benchmark_problem("box2d2r")
     st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
     ext = [16384 + 2 * rad] * 2
-    for bT in (1, 2, 3, 4):
+    for bT in (1, 2):   # the default build has box2d2r b_T 1..2 (build.py CORE)
         g0 = st.describe(ext, {"bT": bT, "vec": 8, "h": 256})
         g1 = st.describe(ext, {"bT": bT, "vec": 8, "h": 256, "direct": 1})
         for k in ("bS", "compute", "halo_loaded", "n_tiles", "n_tb", "n_tb_prime", "stream_overlap"):
