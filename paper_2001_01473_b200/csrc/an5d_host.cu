@@ -754,6 +754,55 @@ an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config
 }
 
 }  // namespace
+// Coefficient table in the run's dtype, with the j-stencil divisor folded in (R-8:
+// the paper's fast-math build turns "/c_0" into a multiply; here it costs
+// nothing at all because 1/c_0 is folded into the taps).
+//   divisor == 1: every coefficient rounded once to nearest (the oracle uses the same values).
+//   divisor != 1: each folded tap is one of the two dtype neighbours of c_d / c_0, chosen so that
+//   the taps' exact sum is as close as possible to sum_d c_d / c_0 (compensated rounding).  Plain
+//   rounding to nearest leaves a systematic bias (sum of taps = 1 + eps) that a T-step run
+//   amplifies T-fold: j2d9pt fp32, T = 1000 drifted 1.1e-5 from the oracle (reading R-8b).
+template <typename T>
+std::vector<T> fold_coefficients(const double* c, size_t n, double divisor) {
+    std::vector<T> out(n);
+    if (divisor == 1.0) {
+        for (size_t k = 0; k < n; ++k) out[k] = (T)c[k];
+        return out;
+    }
+    std::vector<long double> q(n);
+    long double target = 0, sum = 0;
+    for (size_t k = 0; k < n; ++k) {
+        q[k] = (long double)c[k] / (long double)divisor;
+        target += q[k];
+        out[k] = (T)q[k];
+        sum += (long double)out[k];
+    }
+    std::vector<char> flipped(n, 0);
+    for (size_t it = 0; it < n; ++it) {
+        const long double err = sum - target;
+        size_t best = n;
+        long double best_err = fabsl(err);
+        T best_v = 0;
+        for (size_t k = 0; k < n; ++k) {
+            if (flipped[k] || q[k] == (long double)out[k]) continue;
+            // the other neighbour of q[k]
+            const T other = (long double)out[k] < q[k] ? std::nextafter(out[k], (T)INFINITY)
+                                                       : std::nextafter(out[k], (T)-INFINITY);
+            const long double e2 = err - (long double)out[k] + (long double)other;
+            if (fabsl(e2) < best_err) {
+                best_err = fabsl(e2);
+                best = k;
+                best_v = other;
+            }
+        }
+        if (best == n) break;
+        sum += (long double)best_v - (long double)out[best];
+        out[best] = best_v;
+        flipped[best] = 1;
+    }
+    return out;
+}
+
 }  // namespace an5d
 
 using namespace an5d;
@@ -793,16 +842,15 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
         p->elem = dtype == AN5D_F32 ? 4 : 8;
         p->divisor = divisor;
         p->coeffs_folded.resize(n);
-        const double inv = 1.0 / divisor;
-        for (size_t k = 0; k < n; ++k) p->coeffs_folded[k] = divisor == 1.0 ? coeffs[k] : coeffs[k] * inv;
         p->coeffs_dev_t.resize(n * p->elem);
-        for (size_t k = 0; k < n; ++k) {
-            if (dtype == AN5D_F32) {
-                const float f = (float)p->coeffs_folded[k];
-                memcpy(p->coeffs_dev_t.data() + k * 4, &f, 4);
-            } else {
-                memcpy(p->coeffs_dev_t.data() + k * 8, &p->coeffs_folded[k], 8);
-            }
+        if (dtype == AN5D_F32) {
+            const std::vector<float> f = fold_coefficients<float>(coeffs, n, divisor);
+            memcpy(p->coeffs_dev_t.data(), f.data(), n * 4);
+            for (size_t k = 0; k < n; ++k) p->coeffs_folded[k] = f[k];
+        } else {
+            const std::vector<double> f = fold_coefficients<double>(coeffs, n, divisor);
+            memcpy(p->coeffs_dev_t.data(), f.data(), n * 8);
+            for (size_t k = 0; k < n; ++k) p->coeffs_folded[k] = f[k];
         }
         *out = p;
         return AN5D_OK;

@@ -41,20 +41,31 @@ def fp_peak_flops(dtype_bytes: int, n_sm: int = 148, clock_mhz: float = 1965.0) 
 
 
 def roofline(*, ndim, rad, shape, has_div, dtype_bytes, bT, tile_loaded, tile_compute, h, hbm_gbs,
-             fp_peak, rcomp_levels=None):
+             fp_peak):
     """b_T-adjusted roofline in cells/s for a configuration.
 
-    R_read = (prod loaded / prod compute) * (h + 2 bT rad) / h  -- halo + stream-overlap reloads;
-    R_comp = the same redundancy for the computation (this build's kernels compute the full loaded
-    tile at every level, so R_comp = R_read unless `rcomp_levels` says otherwise).
-    roof = min(P eff_ALU / (F R_comp), B bT / (n_w (R_read + 1))); ideal has R = 1.
+    With the logical tile b_i = C_i + 2 b_T rad (the paper's b_S incl. halo), compute
+    region C_i and stream block h:
+      R_read = (prod b / prod C) * (h + 2 b_T rad) / h                  halo + stream-overlap reloads
+      R_comp = (1/b_T) sum_{T=1..b_T} (prod (b_i - 2 T rad) / prod C) * (h + 2 rad (b_T - T)) / h
+               (level T only has to compute its shrinking valid region)
+      roof   = min(P eff_ALU / (F R_comp), B b_T / (n_w (R_read + 1)))
+      ideal  = min(P eff_ALU / F, B b_T / (2 n_w))                      (R = 1)
+    Only useful work is credited: algorithmic bytes per cell-step n_w (R_read + 1) / b_T and FLOPs
+    per cell-step F R_comp.  The kernel's actual redundancy (its loaded window is the logical tile
+    rounded up to whole 16-byte vectors, and it computes that whole window at every level) is
+    reported separately as R_read_kernel / R_comp_kernel.
     """
     import math
     F = flops_per_cell(ndim, rad, shape, has_div)
     eff = eff_alu(ndim, rad, shape, has_div)
-    ratio = math.prod(tile_loaded) / math.prod(tile_compute)
-    r_read = ratio * (h + 2 * bT * rad) / h
-    r_comp = r_read if rcomp_levels is None else rcomp_levels
+    C = list(tile_compute)
+    b = [c + 2 * bT * rad for c in C]
+    pc = math.prod(C)
+    r_read = math.prod(b) / pc * (h + 2 * bT * rad) / h
+    r_comp = sum(math.prod(bi - 2 * T * rad for bi in b) / pc * (h + 2 * rad * (bT - T)) / h
+                 for T in range(1, bT + 1)) / bT
+    r_read_k = math.prod(tile_loaded) / pc * (h + 2 * bT * rad) / h
     comp = fp_peak * eff / (F * r_comp)
     mem = hbm_gbs * 1e9 * bT / (dtype_bytes * (r_read + 1.0))
     ideal_comp = fp_peak * eff / F
@@ -62,6 +73,8 @@ def roofline(*, ndim, rad, shape, has_div, dtype_bytes, bT, tile_loaded, tile_co
     return {
         "roof_cells_s": min(comp, mem), "bound": "alu" if comp < mem else "hbm",
         "comp_cells_s": comp, "hbm_cells_s": mem, "R_read": r_read, "R_comp": r_comp,
+        "R_read_kernel": r_read_k, "R_comp_kernel": r_read_k,
         "ideal_cells_s": min(ideal_comp, ideal_mem), "flops_per_cell": F, "eff_alu": eff,
         "alg_bytes_per_cell_step": dtype_bytes * (r_read + 1.0) / bT,
+        "alg_flops_per_cell_step": F * r_comp,
     }
