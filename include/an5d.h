@@ -115,10 +115,13 @@ typedef struct {
  *     [-r, r]; entry (d) multiplies the neighbour at offset +d: new[x] = sum_d c_d * old[x+d].
  *     STAR tables must have 0 on every entry with more than one non-zero offset component.
  *   divisor: 1.0 = none; j-stencils (j2d5pt, j2d9pt, j3d27pt) divide the sum by c_0 (Table 2).
- *     Applied as in the paper's fast-math build: the reciprocal 1/c_0 is
- *     folded into the coefficients (in double, then rounded once to dtype).
- *   Coefficients are rounded once (round-to-nearest) to dtype.  Copies the table; caller keeps
- *   ownership of `coeffs`.  On success *out owns the plan until an5d_destroy.                  */
+ *     Applied as in the paper's fast-math build: 1/c_0 is folded into
+ *     the coefficients.  Each folded tap is one of the two dtype neighbours of c_d / c_0, chosen
+ *     so that the taps' sum is as close as possible to sum_d c_d / c_0 (compensated rounding,
+ *     DESIGN.md reading R-8b: plain rounding biases the sum and a T-step run amplifies the bias
+ *     T-fold).  divisor == 1: coefficients are rounded once (to nearest) to dtype.
+ *   Copies the table; caller keeps ownership of `coeffs`.  On success *out owns the plan until
+ *   an5d_destroy.                                                                               */
 an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* coeffs,
                         size_t n_coeffs, double divisor, an5d_dtype dtype, an5d_plan** out);
 
@@ -176,6 +179,55 @@ an5d_status an5d_describe(an5d_plan* plan, const int64_t* extents, const an5d_co
  * (bT == 1 with an even T) to *trailing_copy.  Pure host function.                             */
 an5d_status an5d_schedule(int64_t T, int bT, int* degrees, int64_t cap, int64_t* n_sweeps,
                           int* trailing_copy);
+
+/* ---- The paper's performance model (section 5), pure host arithmetic ------------
+ * Thread census of one sweep of degree bT over the whole grid for the PAPER's execution model
+ * (one cell per thread, n_thr = prod b_S threads per block), with the readings of
+ * DESIGN.md "Planner" (SURVEY C-12, C-13): level T = 1..bT computes and reads shared memory on
+ * its valid region prod (b_S_i - 2 T rad) over h + 2 rad (bT - T) planes;
+ * every thread writes shared memory at levels 0..bT-1; global reads n_thr (h + 2 bT rad), global
+ * writes prod C_i * h per (tile, stream block); Table 3 "practical" shared-memory
+ * reads; FLOPs per cell from Table 2 with eff_ALU for k-1 FMA + 1 MUL (+1 MUL for
+ * /c_0); eff_SM with n_SM in the wave count (reading C-12).
+ * time_model = max(time_comp, time_sm, time_gm) / eff_SM.                        */
+typedef struct {
+    int n_sm;                    /* SM count (Table 4: V100 80, P100 56; B200 148)              */
+    int max_threads_per_sm;      /* 2048                                             */
+    double peak_comp_gflops;     /* FP peak of the dtype, GFLOP/s (Table 4)                      */
+    double peak_gm_gbs;          /* measured external-memory throughput, GB/s (Table 4)          */
+    double peak_sm_gbs;          /* measured shared-memory throughput, GB/s (Table 4)            */
+} an5d_device_params;
+
+typedef struct {
+    double th_comp, th_sm_read, th_sm_write, th_gm_read, th_gm_write;  /* per sweep, whole grid  */
+    int64_t n_tb, n_tb_prime;    /* thread blocks per stream block / per sweep    */
+    int n_thr;                   /* threads per block                                            */
+    double flops_per_cell;       /* Table 2                                                      */
+    double eff_alu, eff_sm;
+    double time_comp, time_sm, time_gm, time_model;  /* seconds per sweep of degree bT            */
+    double gflops;               /* useful GFLOP/s: prod I * bT * F / time_model (Table 5 Model) */
+    int bottleneck;              /* 0 compute, 1 shared memory, 2 global memory                  */
+} an5d_model_result;
+
+/* Evaluate the model for one configuration.  interior: I_S_i, outermost (streaming) first.
+ * bS: 2D {b_S_x}, 3D {b_S_y, b_S_x} (tile incl. halo).  Errors: AN5D_ERR_INVALID_ARGUMENT (bad
+ * argument), AN5D_ERR_INFEASIBLE_CONFIG (b_S - 2 bT rad < 1 or n_thr > max_threads_per_sm).   */
+an5d_status an5d_model_paper(int ndim, int radius, an5d_shape shape, int has_divisor, an5d_dtype dtype,
+                             const int64_t* interior, int bT, const int* bS, int64_t h,
+                             const an5d_device_params* dev, an5d_model_result* out);
+
+/* The paper's "Tuned" search: every (bT, bS, h) of the paper's space -- 2D bT 1..16,
+ * bS in {128, 256, 512}, h in {256, 512, 1024}; 3D bT 1..8, bS (y x x) in {16x16, 16x32, 32x32,
+ * 16x64}, h in {128, 256} -- minus the configurations the register rule prunes (P:778-784:
+ * at least bT (2 rad + 1) + bT + 20 registers per thread in single, 2 bT (2 rad + 1) + bT + 30 in
+ * double precision; more than 255 per thread or 65,536 per block is pruned), ranked by the
+ * model's GFLOP/s.  Writes the best min(cap, count) configurations (bT, bS, h filled) and their
+ * predicted GFLOP/s to out_cfg / out_gflops (either may be NULL) and the number of feasible
+ * configurations to *n_feasible.                                                              */
+an5d_status an5d_model_paper_search(int ndim, int radius, an5d_shape shape, int has_divisor,
+                                    an5d_dtype dtype, const int64_t* interior,
+                                    const an5d_device_params* dev, int cap, an5d_config* out_cfg,
+                                    double* out_gflops, int* n_feasible);
 
 /* Number of kernel launches the last an5d_run on this plan issued (for bench gpu_launches).    */
 int64_t an5d_last_launch_count(const an5d_plan* plan);

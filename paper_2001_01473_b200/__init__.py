@@ -60,6 +60,25 @@ class Geometry(ctypes.Structure):
         return out
 
 
+class DeviceParams(ctypes.Structure):
+    _fields_ = [("n_sm", ctypes.c_int), ("max_threads_per_sm", ctypes.c_int), ("peak_comp_gflops", ctypes.c_double),
+                ("peak_gm_gbs", ctypes.c_double), ("peak_sm_gbs", ctypes.c_double)]
+
+
+class ModelResult(ctypes.Structure):
+    _fields_ = [("th_comp", ctypes.c_double), ("th_sm_read", ctypes.c_double), ("th_sm_write", ctypes.c_double),
+                ("th_gm_read", ctypes.c_double), ("th_gm_write", ctypes.c_double), ("n_tb", ctypes.c_int64),
+                ("n_tb_prime", ctypes.c_int64), ("n_thr", ctypes.c_int), ("flops_per_cell", ctypes.c_double),
+                ("eff_alu", ctypes.c_double), ("eff_sm", ctypes.c_double), ("time_comp", ctypes.c_double),
+                ("time_sm", ctypes.c_double), ("time_gm", ctypes.c_double), ("time_model", ctypes.c_double),
+                ("gflops", ctypes.c_double), ("bottleneck", ctypes.c_int)]
+
+    def as_dict(self):
+        d = {name: getattr(self, name) for name, _ in self._fields_}
+        d["bottleneck"] = ("comp", "sm", "gm")[self.bottleneck]
+        return d
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libAN5D.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
@@ -77,6 +96,11 @@ def _load():
         "an5d_tune": (I32, [P, P, P, pi64, pi64, I64, ctypes.POINTER(Config), I32, ctypes.POINTER(Config),
                             ctypes.POINTER(ctypes.c_double), P]),
         "an5d_schedule": (I32, [I64, I32, ctypes.POINTER(ctypes.c_int), I64, pi64, ctypes.POINTER(ctypes.c_int)]),
+        "an5d_model_paper": (I32, [I32, I32, I32, I32, I32, pi64, I32, ctypes.POINTER(ctypes.c_int), I64,
+                                   ctypes.POINTER(DeviceParams), ctypes.POINTER(ModelResult)]),
+        "an5d_model_paper_search": (I32, [I32, I32, I32, I32, I32, pi64, ctypes.POINTER(DeviceParams), I32,
+                                          ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_int)]),
         "an5d_last_launch_count": (I64, [P]),
         "an5d_destroy": (I32, [P]),
         "an5d_last_error": (ctypes.c_char_p, []),
@@ -113,8 +137,8 @@ def loaded() -> bool:
     return _LazyLib._h is not None
 
 EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
-                    "an5d_describe", "an5d_schedule", "an5d_last_launch_count", "an5d_destroy",
-                    "an5d_last_error", "an5d_version")
+                    "an5d_describe", "an5d_schedule", "an5d_model_paper", "an5d_model_paper_search",
+                    "an5d_last_launch_count", "an5d_destroy", "an5d_last_error", "an5d_version")
 
 
 def _check(st: int):
@@ -151,6 +175,39 @@ def schedule(T: int, bT: int):
     buf = (ctypes.c_int * max(1, n.value))()
     _check(_lib.an5d_schedule(int(T), int(bT), buf, n.value, ctypes.byref(n), ctypes.byref(tc)))
     return [buf[i] for i in range(n.value)], bool(tc.value)
+
+
+def _devparams(dev: dict) -> DeviceParams:
+    d = DeviceParams()
+    d.n_sm = int(dev["n_sm"])
+    d.max_threads_per_sm = int(dev.get("max_threads_per_sm", 2048))
+    d.peak_comp_gflops = float(dev["comp"])
+    d.peak_gm_gbs = float(dev["gm"])
+    d.peak_sm_gbs = float(dev["sm"])
+    return d
+
+
+def model_paper(ndim, rad, shape, has_div, dtype, interior, bT, bS, h, dev) -> dict:
+    """The paper's section-5 model (an5d_model_paper) for one configuration.
+    dev: {"n_sm", "comp" (GFLOP/s of the dtype), "gm" (GB/s), "sm" (GB/s)} (Table 4)."""
+    out = ModelResult()
+    bs = (ctypes.c_int * 2)(*(list(bS) + [0, 0])[:2])
+    dt = F32 if dtype in (torch.float32, F32) else F64
+    _check(_lib.an5d_model_paper(ndim, rad, shape, int(bool(has_div)), dt, _i64(interior), int(bT), bs, int(h),
+                                 ctypes.byref(_devparams(dev)), ctypes.byref(out)))
+    return out.as_dict()
+
+
+def model_paper_search(ndim, rad, shape, has_div, dtype, interior, dev, top_k=5):
+    """The paper's "Tuned" search space ranked by the model (an5d_model_paper_search):
+    returns (list of (config dict, GFLOP/s) best first, number of feasible configurations)."""
+    cfgs = (Config * max(1, top_k))()
+    gf = (ctypes.c_double * max(1, top_k))()
+    n = ctypes.c_int()
+    dt = F32 if dtype in (torch.float32, F32) else F64
+    _check(_lib.an5d_model_paper_search(ndim, rad, shape, int(bool(has_div)), dt, _i64(interior),
+                                        ctypes.byref(_devparams(dev)), int(top_k), cfgs, gf, ctypes.byref(n)))
+    return [(cfgs[i].as_dict(), gf[i]) for i in range(min(top_k, n.value))], n.value
 
 
 def vec_width(dtype) -> int:

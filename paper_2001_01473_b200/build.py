@@ -239,7 +239,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
     t0 = time.time()
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     os.makedirs(OBJ, exist_ok=True)
-    srcs = generate() + [os.path.join(CSRC, "an5d_host.cu")]
+    srcs = generate() + [os.path.join(CSRC, "an5d_host.cu"), os.path.join(CSRC, "an5d_model.cu")]
     hdr = {k: _header_digest(k) for k in DEPS}
     jobs = jobs or max(1, os.cpu_count() or 1)
     # heavy instances (3D, box, high b_T) first so the longest compiles do not end up in the tail
@@ -263,7 +263,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
     with open(stamp, "w") as f:
         f.write(digest)
     if verbose:
-        print(f"built {LIB} ({len(srcs) - 1} kernel instances, {jobs} jobs, {time.time() - t0:.0f} s)",
+        print(f"built {LIB} ({len(srcs) - 2} kernel instances, {jobs} jobs, {time.time() - t0:.0f} s)",
               file=sys.stderr)
     return LIB
 

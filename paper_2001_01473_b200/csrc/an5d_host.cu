@@ -46,6 +46,11 @@ int64_t round_up(int64_t a, int64_t m) { return cdiv(a, m) * m; }
 
 }  // namespace
 
+an5d_status set_error(an5d_status s, const char* msg) {
+    g_err = msg;
+    return s;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Plan
 // ---------------------------------------------------------------------------------------------
