@@ -254,6 +254,7 @@ def main():
     ap.add_argument("--bt", type=int, default=0, help="force b_T (0 = planner)")
     ap.add_argument("--vec", type=int, default=0)
     ap.add_argument("--h", type=int, default=0)
+    ap.add_argument("--nthr", type=int, default=0, help="threads per block of the kernel layout (0 = planner)")
     ap.add_argument("--direct", type=int, default=0, choices=[0, 1],
                     help="1 = partial sums OFF: the non-associative direct-gather kernels (BASELINE config 4)")
     ap.add_argument("--no-tune", action="store_true", help="planner model only (no measured top-5 pick)")
@@ -324,7 +325,7 @@ def run_an5d(args):
     ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
     ext = (n + 2 * rad,) * ndim
     st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
-    hint = {"bT": args.bt, "vec": args.vec, "h": args.h, "direct": args.direct}
+    hint = {"bT": args.bt, "vec": args.vec, "h": args.h, "direct": args.direct, "n_thr": args.nthr}
     a = an5d.empty_grid(ext, rad, dtype, dev)
     b = an5d.empty_grid(ext, rad, dtype, dev)
     fill_uniform(a, inputs.DEFAULT_SEED, ext)
@@ -489,7 +490,7 @@ def run_an5d(args):
         "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if dtype == torch.float32 else "f64", "data": "synthetic",
         "config": {"workload": args.workload, "stencil": name, "grid": list(ext), "T": T, "bT": cfg["bT"],
-                   "vec": cfg["vec"], "h": cfg["h"], "partial_sums": "off" if cfg.get("direct") else "on",
+                   "vec": cfg["vec"], "h": cfg["h"], "n_thr": cfg["n_thr"], "partial_sums": "off" if cfg.get("direct") else "on",
                    "planner": "model" if args.no_tune else "model top-5, measured pick (P:784-793)",
                    "bS": geom["bS"][:nb], "bS_loaded": geom["bS_loaded"][:nb],
                    "parallelism": "1 GPU", "l2": f"inputs larger than L2 ({a.numel() * a.element_size() / 2**30:.2f} GiB per grid buffer > 126 MB)",

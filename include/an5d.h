@@ -81,6 +81,10 @@ typedef struct {
                      /*    at once -- kept for the partial-sum on/off comparison (BASELINE       */
                      /*    config 4).  2D only (else AN5D_ERR_UNSUPPORTED); the planner never    */
                      /*    picks 1 by itself.  Values other than 0/1: AN5D_ERR_INVALID_ARGUMENT. */
+    int n_thr;       /* threads per thread block of the kernel layout (P:316 n_thr); with bS it    */
+                     /* selects the layout: 2D 32 (one warp per tile); 3D 256 (16 x 16 threads, */
+                     /* 64-wide tiles) or 512 (32 x 16 threads: 64-wide fp64 tiles at half the  */
+                     /* registers per thread, or 128-wide fp32 tiles).  0 = planner / default.  */
 } an5d_config;
 
 /* Bookkeeping of one sweep of degree bT under `cfg` (bit-exact).        */

@@ -35,10 +35,11 @@ class AN5DError(RuntimeError):
 
 class Config(ctypes.Structure):
     _fields_ = [("bT", ctypes.c_int), ("bS", ctypes.c_int * 2), ("h", ctypes.c_int64), ("vec", ctypes.c_int),
-                ("direct", ctypes.c_int)]
+                ("direct", ctypes.c_int), ("n_thr", ctypes.c_int)]
 
     def as_dict(self):
-        return {"bT": self.bT, "bS": list(self.bS), "h": self.h, "vec": self.vec, "direct": self.direct}
+        return {"bT": self.bT, "bS": list(self.bS), "h": self.h, "vec": self.vec, "direct": self.direct,
+                "n_thr": self.n_thr}
 
 
 class Geometry(ctypes.Structure):
@@ -164,6 +165,7 @@ def _cfg(cfg) -> Config | None:
     c.h = int(cfg.get("h", 0))
     c.vec = int(cfg.get("vec", 0))
     c.direct = int(cfg.get("direct", 0))
+    c.n_thr = int(cfg.get("n_thr", 0) or 0)
     return c
 
 

@@ -59,6 +59,17 @@ CORE = {
 }
 # partial sums OFF (direct gather, BASELINE config 4 = box2d2r fp32): vec 8 and 4, b_T 1..2
 CORE_DIRECT = {(2, 0, 1, 2): [(8, 2), (4, 2)]}
+# 3D 512-thread layouts (kernel3d.cuh Kernel3DTraits): "t32x2" = 32 x 16 threads with 2-cell patch
+# rows (fp64: 64-wide tiles at half the registers per thread, twice the warps per SM; rad <= 2),
+# "t32x4" = 32 x 16 threads with 4-cell rows (fp32: 128-wide tiles, less x-halo redundancy).
+# Key as CORE -> [(vec, max b_T, layout)].
+CORE_LAYOUTS = {
+    (3, 1, 0, 1): [(2, 3, "t32x2")], (3, 1, 0, 2): [(2, 2, "t32x2")],
+    (3, 1, 1, 1): [(2, 2, "t32x2")],
+    (3, 0, 0, 1): [(2, 4, "t32x4")], (3, 0, 0, 2): [(2, 2, "t32x4")], (3, 0, 0, 3): [(2, 1, "t32x4")],
+    (3, 0, 0, 4): [(2, 1, "t32x4")], (3, 0, 1, 1): [(2, 2, "t32x4")],
+}
+LAYOUTS = {"": (16, 4), "t32x2": (32, 2), "t32x4": (32, 4)}   # layout -> (TXT, VX)
 
 
 def full_instances():
@@ -90,7 +101,7 @@ def full_instances():
                     out.append((3, 0, shape, rad, bT, 2))
                 if rad * bT <= 4:
                     out.append((3, 1, shape, rad, bT, 2))
-    return [i if len(i) == 7 else i + (1,) for i in out]
+    return [(i + ("",)) if len(i) == 7 else i + (1, "") for i in out]
 
 
 def core_instances():
@@ -98,13 +109,16 @@ def core_instances():
     for tab, assoc in ((CORE, 1), (CORE_DIRECT, 0)):
         for (ndim, dtype, shape, rad), lst in tab.items():
             for vec, bmax in lst:
-                out += [(ndim, dtype, shape, rad, bT, vec, assoc) for bT in range(1, bmax + 1)]
+                out += [(ndim, dtype, shape, rad, bT, vec, assoc, "") for bT in range(1, bmax + 1)]
+    for (ndim, dtype, shape, rad), lst in CORE_LAYOUTS.items():
+        for vec, bmax, lay in lst:
+            out += [(ndim, dtype, shape, rad, bT, vec, 1, lay) for bT in range(1, bmax + 1)]
     return out
 
 
 def instances():
-    """(ndim, dtype, shape, rad, bT, vec, assoc) tuples; dtype 0=f32 1=f64, shape 0=star 1=box,
-    assoc 1 = partial sums, 0 = direct gather.  Default: core_instances(); AN5D_FULL_BUILD=1: the
+    """(ndim, dtype, shape, rad, bT, vec, assoc, layout) tuples; dtype 0=f32 1=f64, shape 0=star
+    1=box, assoc 1 = partial sums, 0 = direct gather, layout "" or a 3D LAYOUTS key.  Default: core_instances(); AN5D_FULL_BUILD=1: the
     full b_T-sweep matrix (plus the core set); AN5D_DEV_INSTANCES: a development subset."""
     out = core_instances()
     if os.environ.get("AN5D_FULL_BUILD", "") not in ("", "0"):
@@ -120,9 +134,9 @@ def instances():
     return out
 
 
-def inst_name(ndim, dtype, shape, rad, bT, vec, assoc):
+def inst_name(ndim, dtype, shape, rad, bT, vec, assoc, layout=""):
     return (f"inst_{ndim}d_{'f64' if dtype else 'f32'}_{'box' if shape else 'star'}_r{rad}"
-            f"_bt{bT}_v{vec}{'' if assoc else '_direct'}")
+            f"_bt{bT}_v{vec}{'' if assoc else '_direct'}{'_' + layout if layout else ''}")
 
 
 def _regcaps():
@@ -137,10 +151,12 @@ def generate():
     caps = _regcaps()
     files = []
     for inst in instances():
-        (ndim, dtype, shape, rad, bT, vec, assoc) = inst
+        (ndim, dtype, shape, rad, bT, vec, assoc, layout) = inst
         T = "double" if dtype else "float"
         name = inst_name(*inst)
         targs = f"{T}, {rad}, {bT}, {vec}, {'true' if shape else 'false'}" + ("" if assoc else ", false")
+        if layout:
+            targs += ", %d, %d" % LAYOUTS[layout]
         fn = "make_instance2d" if ndim == 2 else "make_instance3d"
         lines = ["// GENERATED by paper_2001_01473_b200/build.py -- one kernel instance."]
         if name in caps:
@@ -223,8 +239,12 @@ def _compile(src, nvcc, hdr):
         regs = max([int(v) for v in re.findall(r"Used (\d+) registers", r.stderr)] or [255])
         if known or "AN5D_MINB_FORCE" in " ".join(NVCC_FLAGS) or _spill_bytes(r.stderr) <= SPILL_LIMIT or regs > 168:
             break
-        # next register budget: 128 -> 168 (2D: 12 one-warp blocks) -> 255; 3D: 128 -> 255
-        cap = 12 if (regs <= 128 and "_2d_" in base) else 1
+        # next register budget: 128 -> 168 (2D: 12 one-warp blocks) -> 255; 3D: 128 -> 255.  A
+        # 512-thread 3D layout is already at one block (<= 128 registers): nothing left to relax
+        nxt = 12 if (regs <= 128 and "_2d_" in base) else 1
+        if nxt == cap or "_t32x" in base:
+            break
+        cap = nxt
     if not known:
         print(f"build.py: {base} not in regcaps.json; calibrated cap = {cap} (add it to the table)",
               file=sys.stderr)

@@ -105,12 +105,31 @@ void make_schedule(int64_t T, int bT, std::vector<int>& deg, bool& trailing_copy
     }
 }
 
-const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0) {
+// Kernel instance for (b_T, vec, direct) with a loaded tile width `tile_x` (0 = any) and
+// `n_thr` threads per block (0 = any).  Among several matches the narrowest tile with the fewest
+// threads is the default (the round-1 layouts), so a config that names neither keeps them.
+const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0, int tile_x = 0, int n_thr = 0) {
+    const Instance* best = nullptr;
     for (const Instance& i : registry())
-        if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad &&
-            i.bT == bT && i.vec == vec && i.assoc == (direct ? 0 : 1))
-            return &i;
-    return nullptr;
+        if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad && i.bT == bT &&
+            i.vec == vec && i.assoc == (direct ? 0 : 1) && (!tile_x || i.tile_x_loaded == tile_x) &&
+            (!n_thr || i.threads == n_thr))
+            if (!best || std::make_pair(i.tile_x_loaded, i.threads) < std::make_pair(best->tile_x_loaded, best->threads))
+                best = &i;
+    return best;
+}
+
+// Loaded x width of the tile a configuration names through its logical b_S (0 = not named): the
+// logical halo b_T rad per side rounded up to whole 16-byte vectors (sweep_geometry).
+int cfg_tile_x(const Plan& p, const an5d_config& c) {
+    const int bs = c.bS[p.ndim - 2];
+    if (!bs || !c.bT) return 0;
+    const int A = (int)(16 / p.elem), hl = c.bT * p.rad;
+    return bs - 2 * hl + 2 * ((hl + A - 1) / A) * A;
+}
+
+const Instance* find_instance(const Plan& p, int bT, const an5d_config& c) {
+    return find_instance(p, bT, c.vec, c.direct, cfg_tile_x(p, c), c.n_thr);
 }
 
 int max_bT_for(const Plan& p, int vec) {
@@ -409,10 +428,13 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
         if (inst.assoc != (direct ? 0 : 1)) continue;
         if (hint && hint->bT && inst.bT != hint->bT) continue;
         if (hint && hint->vec && inst.vec != hint->vec) continue;
+        if (hint && hint->n_thr && inst.threads != hint->n_thr) continue;
+        if (hint && cfg_tile_x(p, *hint) && inst.tile_x_loaded != cfg_tile_x(p, *hint)) continue;
         if (T > 0 && inst.bT > T) continue;
-        // every reduced degree the schedule may need must exist with the same vec
+        // every reduced degree the schedule may need must exist with the same layout
         bool ok = true;
-        for (int d = 1; d < inst.bT && ok; ++d) ok = find_instance(p, d, inst.vec, direct) != nullptr;
+        for (int d = 1; d < inst.bT && ok; ++d)
+            ok = find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, inst.threads) != nullptr;
         if (!ok) continue;
         std::vector<int64_t> hs;
         if (hint && hint->h) {
@@ -438,6 +460,12 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
             c.bT = inst.bT;
             c.vec = inst.vec;
             c.h = h;
+            c.n_thr = inst.threads;
+            {   // logical tile b_S = compute region + 2 b_T rad (names the layout, cfg_tile_x)
+                SweepGeom g{};
+                sweep_geometry(p, inst, dm, inst.bT, h, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g);
+                for (int i = 0; i < p.ndim - 1; ++i) c.bS[i] = g.C[i] + 2 * inst.bT * p.rad;
+            }
             c.direct = direct;
             out.emplace_back(t, c);
         }
@@ -578,7 +606,7 @@ an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src,
 an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, int d, const an5d_config& cfg,
                          int64_t g_off, int64_t gE0, int64_t out_lo, int64_t out_hi, int32_t* wc,
                          cudaStream_t st) {
-    const Instance* inst = find_instance(p, d, cfg.vec, cfg.direct);
+    const Instance* inst = find_instance(p, d, cfg);
     if (!inst) return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for degree %d vec %d", d, cfg.vec);
     SweepGeom g{};
     an5d_status s = sweep_geometry(p, *inst, dm, d, cfg.h, g_off, gE0, out_lo, out_hi, g);
@@ -725,7 +753,8 @@ an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config
             if (h) hint.h = h;
         }
     }
-    if (hint.bT < 0 || hint.vec < 0 || hint.h < 0) return fail(AN5D_ERR_INVALID_ARGUMENT, "negative config field");
+    if (hint.bT < 0 || hint.vec < 0 || hint.h < 0 || hint.n_thr < 0 || hint.bS[0] < 0 || hint.bS[1] < 0)
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "negative config field");
     if (hint.direct != 0 && hint.direct != 1) return fail(AN5D_ERR_INVALID_ARGUMENT, "direct must be 0 or 1");
     if (hint.bT && hint.vec && hint.h) {
         c = hint;
@@ -735,14 +764,16 @@ an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config
     }
     if (c.direct && p.ndim != 2)
         return fail(AN5D_ERR_UNSUPPORTED, "direct (non-associative) variant is 2D only");
-    if (!find_instance(p, c.bT, c.vec, c.direct))
-        return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for ndim=%d rad=%d shape=%d dtype=%d bT=%d vec=%d",
-                    p.ndim, p.rad, p.shape, p.dtype, c.bT, c.vec);
+    const Instance* inst = find_instance(p, c.bT, c);
+    if (!inst)
+        return fail(AN5D_ERR_UNSUPPORTED,
+                    "no kernel instance for ndim=%d rad=%d shape=%d dtype=%d bT=%d vec=%d bS=(%d,%d) n_thr=%d", p.ndim,
+                    p.rad, p.shape, p.dtype, c.bT, c.vec, c.bS[0], c.bS[1], c.n_thr);
     for (int d = 1; d < c.bT; ++d)
-        if (!find_instance(p, d, c.vec, c.direct))
+        if (!find_instance(p, d, c.vec, c.direct, inst->tile_x_loaded, inst->threads))
             return fail(AN5D_ERR_UNSUPPORTED, "no reduced-degree instance d=%d for vec %d", d, c.vec);
+    c.n_thr = inst->threads;
     // logical tile b_S reported back
-    const Instance* inst = find_instance(p, c.bT, c.vec, c.direct);
     SweepGeom g{};
     an5d_status s = sweep_geometry(p, *inst, dm, c.bT, c.h ? c.h : dm.E[0], 0, dm.E[0], p.rad, dm.E[0] - p.rad, g);
     if (s != AN5D_OK) return s;
@@ -912,7 +943,7 @@ an5d_status an5d_plan_config(an5d_plan* p, const int64_t* extents, int64_t T, co
 
 // The paper's tuning procedure: rank every configuration with the model, run the top
 // few on the GPU, keep the fastest.  Candidates are the best stream-block length of each of the
-// top_k distinct (b_T, vec) pairs; each is timed over two sweeps (after one warm-up sweep) reading
+// top_k distinct (b_T, vec, layout) triples; each is timed over two sweeps (after one warm-up sweep) reading
 // grid_in and writing grid_out.  Blocking: synchronises cuda_stream.
 an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const int64_t* extents,
                       const int64_t* pitches, int64_t T, const an5d_config* hint, int top_k, an5d_config* out,
@@ -934,7 +965,9 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         std::vector<an5d_config> cand;
         for (const auto& r : ranked) {
             bool seen = false;
-            for (const auto& c : cand) seen = seen || (c.bT == r.second.bT && c.vec == r.second.vec);
+            for (const auto& c : cand)
+                seen = seen || (c.bT == r.second.bT && c.vec == r.second.vec && c.n_thr == r.second.n_thr &&
+                                c.bS[0] == r.second.bS[0] && c.bS[1] == r.second.bS[1]);
             if (!seen) cand.push_back(r.second);
             if ((int)cand.size() >= top_k) break;
         }
@@ -1014,7 +1047,7 @@ an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_confi
         if (s != AN5D_OK) return s;
         an5d_config c{};
         if ((s = resolve_config(*p, dm, 0, cfg, c)) != AN5D_OK) return s;
-        const Instance* inst = find_instance(*p, c.bT, c.vec, c.direct);
+        const Instance* inst = find_instance(*p, c.bT, c);
         SweepGeom g{};
         if ((s = sweep_geometry(*p, *inst, dm, c.bT, c.h, 0, dm.E[0], p->rad, dm.E[0] - p->rad, g)) != AN5D_OK)
             return s;
@@ -1126,7 +1159,7 @@ an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t*
         make_schedule(T, c.bT, deg, tc);
         // validate every sweep's geometry before the first launch (no partial writes on error)
         for (int d : deg) {
-            const Instance* inst = find_instance(*p, d, c.vec, c.direct);
+            const Instance* inst = find_instance(*p, d, c);
             SweepGeom g{};
             if ((s = sweep_geometry(*p, *inst, dm, d, c.h, 0, dm.E[0], p->rad, dm.E[0] - p->rad, g)) != AN5D_OK)
                 return s;

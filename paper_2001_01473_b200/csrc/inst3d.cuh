@@ -6,10 +6,10 @@
 
 namespace an5d {
 
-template <typename T, int R, int BT, int VY, bool BOX>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX>
 cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap& tmap, int64_t blocks,
                      cudaStream_t st) {
-    using K = Kernel3DTraits<T, R, BT, VY>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
     constexpr int N = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
     Coeffs3D<T, R> cf;
     const T* c = static_cast<const T*>(coeffs);
@@ -17,7 +17,7 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
         if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
         else cf.c[i] = c[i];
     }
-    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX>;
+    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (!attr_set) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
@@ -27,15 +27,15 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
     return cudaGetLastError();
 }
 
-template <typename T, int R, int BT, int VY, bool BOX>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4>
 Instance make_instance3d() {
-    using K = Kernel3DTraits<T, R, BT, VY>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
     Instance i{};
     i.ndim = 3; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
     i.rad = R; i.bT = BT; i.vec = VY; i.assoc = 1;
     i.launch2d = nullptr;
-    i.launch3d = &launch3d<T, R, BT, VY, BOX>;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX>);
+    i.launch3d = &launch3d<T, R, BT, VY, BOX, TXT, VX>;
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX>);
     i.fn_edge = i.fn_interior;
     i.threads = K::kThreads;
     i.tile_x_loaded = K::kTX;

@@ -41,10 +41,18 @@ namespace an5d {
 
 constexpr int kPrefetch3D = 3;
 
-template <typename T, int R, int BT, int VY>
+// Thread layout (TXT_ x 16 threads, patch VY x VX_ cells per thread):
+//   TXT_ = 16, VX_ = 4: 256 threads, 64 x 16 VY tile plane (the default; fp32 and fp64);
+//   TXT_ = 32, VX_ = 2: 512 threads, 64 x 16 VY tile -- fp64 with half the registers per thread,
+//                       so twice the warps per SM (one 16-byte vector per patch row);
+//   TXT_ = 32, VX_ = 4: 512 threads, 128 x 16 VY tile -- a wider tile: less x-halo redundancy
+//                       (the planner's b_S choice).
+template <typename T, int R, int BT, int VY, int TXT_ = 16, int VX_ = 4>
 struct Kernel3DTraits {
-    static constexpr int VX = 4;
-    static constexpr int TXT = 16, TYT = 16;
+    static constexpr int VX = VX_;
+    static constexpr int TXT = TXT_, TYT = 16;
+    static_assert(VX >= R, "x halo: a thread's rad neighbour cells must come from one adjacent thread");
+    static_assert(VX % VecOf<T>::A == 0, "patch rows are whole 16-byte vectors");
     static constexpr int kThreads = TXT * TYT;
     static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // tile plane (loaded), x by y
     static constexpr int PROWS = kTY + 2 * R;               // staged rows (R garbage pad rows per side)
@@ -127,10 +135,10 @@ struct Unit3D {
 template <typename T, int R>
 using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * (2 * R + 1)>;
 
-template <typename T, int R, int BT, int VY, bool BOX, bool EDGE>
+template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_>
 __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
                                              const Unit3D& g, const void* tmap) {
-    using K = Kernel3DTraits<T, R, BT, VY>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX_>;
     using LN = Lane<T, K::VX>;
     using E = typename LN::E;
     constexpr int NE = LN::NE;              // elements per patch row
@@ -487,11 +495,12 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 }
 
 // resident blocks per SM the register budget is shaped for: small fp32 patches (VY <= 2) fit two
-// blocks (<= 128 registers/thread), so one block's barrier and latency stalls overlap the other's;
-// fp64 (twice the registers per cell) and high-order box keep one block and up to 255 registers
-// (build.py lowers the cap with AN5D_MINB_CAP when ptxas reports spills at 128 registers)
-template <typename T, int VY, int R, bool BOX> constexpr int min_blocks_3d() {
-    constexpr int m = (sizeof(T) == 4 && VY <= 2 && !(BOX && R >= 2)) ? 2 : 1;
+// 256-thread blocks (<= 128 registers/thread), so one block's barrier and latency stalls overlap
+// the other's; fp64 (twice the registers per cell) and high-order box keep one block and up to 255
+// registers; 512-thread layouts one block at <= 128 registers (build.py / regcaps.json lower the
+// cap with AN5D_MINB_CAP where ptxas reports spills)
+template <typename T, int VY, int R, bool BOX, int TXT> constexpr int min_blocks_3d() {
+    constexpr int m = (TXT == 16 && sizeof(T) == 4 && VY <= 2 && !(BOX && R >= 2)) ? 2 : 1;
 #ifdef AN5D_MINB_CAP
     return m < AN5D_MINB_CAP ? m : AN5D_MINB_CAP;
 #else
@@ -499,10 +508,10 @@ template <typename T, int VY, int R, bool BOX> constexpr int min_blocks_3d() {
 #endif
 }
 
-template <typename T, int R, int BT, int VY, bool BOX>
-__global__ void __launch_bounds__(256, min_blocks_3d<T, VY, R, BOX>())
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4>
+__global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
 an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
-    using K = Kernel3DTraits<T, R, BT, VY>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* const smem = reinterpret_cast<T*>(smem_raw);
     const int64_t unit = blockIdx.x;
@@ -538,8 +547,8 @@ an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf, const __grid_constant
     // z-ring planes and the array's z ends are handled by both variants (uniform per-step checks);
     // the EDGE variant is only for tiles whose window touches the x/y ring or the array end
     if (threadIdx.x == 0) tma_prefetch_desc(&tmap);
-    if (g.ring_xy) sweep3d_unit<T, R, BT, VY, BOX, true>(a, cf, smem, g, &tmap);
-    else sweep3d_unit<T, R, BT, VY, BOX, false>(a, cf, smem, g, &tmap);
+    if (g.ring_xy) sweep3d_unit<T, R, BT, VY, BOX, true, TXT, VX>(a, cf, smem, g, &tmap);
+    else sweep3d_unit<T, R, BT, VY, BOX, false, TXT, VX>(a, cf, smem, g, &tmap);
 }
 
 }  // namespace an5d

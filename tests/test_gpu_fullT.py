@@ -46,7 +46,8 @@ def test_full_T_parity_planner_config(an5d, name, dtype):
     full = (16384 + 2 * rad,) * 2 if ndim == 2 else (512 + 2 * rad,) * 3
     st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
     pick = st.plan_config(full, 1000)                       # the planner's (b_T, vec) at BASELINE size
-    cfg = st.plan_config(ext, T, {"bT": pick["bT"], "vec": pick["vec"]})   # h for this grid
+    cfg = st.plan_config(ext, T, {"bT": pick["bT"], "vec": pick["vec"], "n_thr": pick["n_thr"],
+                                  "bS": pick["bS"]})                       # same layout; h for this grid
     g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
     a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
     b = an5d.empty_grid(ext, rad, dtype)

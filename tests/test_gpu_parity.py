@@ -46,25 +46,30 @@ def gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg=None):
 
 def small_ext(ndim, rad):
     # spans several tiles in every blocked dim + ragged tails: 2D >= 5 vec-8 tiles across (256-cell
-    # tiles), so interior (non-EDGE) units run too; 3D 64 x 32 tiles: >= 4 across in y and x
-    return (61 + 2 * rad, 1301 + 2 * rad) if ndim == 2 else (23 + 2 * rad, 131 + 2 * rad, 269 + 2 * rad)
+    # tiles), so interior (non-EDGE) units run too; 3D: >= 4 tiles across in y and x (64 x 32 and
+    # 128 x 32 tiles)
+    return (61 + 2 * rad, 1301 + 2 * rad) if ndim == 2 else (23 + 2 * rad, 131 + 2 * rad, 509 + 2 * rad)
 
 
 def configs_for(an5d, st, ext, ndim, direct=0):
-    """A spread of available (bT, vec) configurations for this stencil, with short stream blocks so
-    several stream blocks (and interior + edge launches) are exercised."""
+    """A spread of available (bT, vec, layout) configurations for this stencil, with short stream
+    blocks so several stream blocks (and interior + edge units) are exercised.  3D: the default
+    256-thread layout and the 512-thread layouts (n_thr = 512: 64-wide fp64 / 128-wide fp32
+    tiles) where they are built."""
     out = []
-    for vec in (1, 2, 4, 8):
-        bts = []
-        for bT in range(1, 11):
-            try:
-                st.describe(ext, {"bT": bT, "vec": vec, "h": 16, "direct": direct})
-                bts.append(bT)
-            except an5d.AN5DError:
-                pass
-        if bts:
-            picks = sorted({bts[0], bts[len(bts) // 2], bts[-1]})
-            out += [{"bT": b, "vec": vec, "h": 16 if ndim == 2 else 8, "direct": direct} for b in picks]
+    for n_thr in ((0,) if ndim == 2 else (256, 512)):
+        for vec in (1, 2, 4, 8):
+            bts = []
+            for bT in range(1, 11):
+                try:
+                    st.describe(ext, {"bT": bT, "vec": vec, "h": 16, "direct": direct, "n_thr": n_thr})
+                    bts.append(bT)
+                except an5d.AN5DError:
+                    pass
+            if bts:
+                picks = sorted({bts[0], bts[len(bts) // 2], bts[-1]})
+                out += [{"bT": b, "vec": vec, "h": 16 if ndim == 2 else 8, "direct": direct, "n_thr": n_thr}
+                        for b in picks]
     return out
 
 
@@ -359,12 +364,14 @@ def test_stream_block_runs(an5d, name, dtype, cfg, monkeypatch):
     ("star3d1r", torch.float32, {"bT": 3, "h": 4, "vec": 2}),
     ("box3d1r", torch.float64, {"bT": 2, "h": 4, "vec": 2}),
     ("star3d2r", torch.float32, {"bT": 2, "h": 4, "vec": 2}),
+    ("star3d1r", torch.float64, {"bT": 3, "h": 4, "vec": 2, "n_thr": 512}),
+    ("star3d2r", torch.float32, {"bT": 2, "h": 4, "vec": 2, "n_thr": 512}),
 ])
 def test_stream_block_runs_3d(an5d, name, dtype, cfg, monkeypatch):
     """3D run schedule (build_runs_3d): long runs forced by shaping the table for 2 blocks; oracle
     parity, bit-identical to the plain schedule, exact-integer mode, store counts once."""
     ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
-    ext = (41 + 2 * rad, 150 + 2 * rad, 290 + 2 * rad)   # >= 4 tiles in y and x (interior tiles), ~10 stream blocks
+    ext = (41 + 2 * rad, 150 + 2 * rad, 530 + 2 * rad)   # >= 4 tiles in y and x (interior tiles), ~10 stream blocks
     g = inputs.global_grid(78, ext)
     T = 2 * cfg["bT"] + 1
     monkeypatch.setenv("AN5D_RUN_WARPS", "2")
