@@ -69,7 +69,14 @@ CORE_LAYOUTS = {
     (3, 0, 0, 1): [(2, 4, "t32x4")], (3, 0, 0, 2): [(2, 2, "t32x4")], (3, 0, 0, 3): [(2, 1, "t32x4")],
     (3, 0, 0, 4): [(2, 1, "t32x4")], (3, 0, 1, 1): [(2, 2, "t32x4")],
 }
-LAYOUTS = {"": (16, 4), "t32x2": (32, 2), "t32x4": (32, 4)}   # layout -> (TXT, VX)
+LAYOUTS = {"": (16, 4), "t32x2": (32, 2), "t32x4": (32, 4)}   # 3D layout -> (TXT, VX)
+# 2D level split "w2" (kernel2d.cuh Split2D): two warps per tile, warp 0 levels 1..b_T/2 with the
+# staging, warp 1 the rest with the store -- half the partial-sum registers per warp.  b_T 1 has
+# nothing to split: the reduced-degree sweep of degree 1 uses the one-warp instance.
+CORE_SPLIT = {
+    (2, 0, 0, 1): [(8, 10)], (2, 0, 0, 2): [(8, 6)], (2, 0, 1, 1): [(8, 6)],
+    (2, 1, 0, 1): [(4, 8)], (2, 1, 0, 2): [(4, 5)],
+}
 
 
 def full_instances():
@@ -113,6 +120,9 @@ def core_instances():
     for (ndim, dtype, shape, rad), lst in CORE_LAYOUTS.items():
         for vec, bmax, lay in lst:
             out += [(ndim, dtype, shape, rad, bT, vec, 1, lay) for bT in range(1, bmax + 1)]
+    for (ndim, dtype, shape, rad), lst in CORE_SPLIT.items():
+        for vec, bmax in lst:
+            out += [(ndim, dtype, shape, rad, bT, vec, 1, "w2") for bT in range(2, bmax + 1)]
     return out
 
 
@@ -155,7 +165,9 @@ def generate():
         T = "double" if dtype else "float"
         name = inst_name(*inst)
         targs = f"{T}, {rad}, {bT}, {vec}, {'true' if shape else 'false'}" + ("" if assoc else ", false")
-        if layout:
+        if layout == "w2":
+            targs += ", true, 2"
+        elif layout:
             targs += ", %d, %d" % LAYOUTS[layout]
         fn = "make_instance2d" if ndim == 2 else "make_instance3d"
         lines = ["// GENERATED by paper_2001_01473_b200/build.py -- one kernel instance."]
@@ -239,10 +251,17 @@ def _compile(src, nvcc, hdr):
         regs = max([int(v) for v in re.findall(r"Used (\d+) registers", r.stderr)] or [255])
         if known or "AN5D_MINB_FORCE" in " ".join(NVCC_FLAGS) or _spill_bytes(r.stderr) <= SPILL_LIMIT or regs > 168:
             break
-        # next register budget: 128 -> 168 (2D: 12 one-warp blocks) -> 255; 3D: 128 -> 255.  A
-        # 512-thread 3D layout is already at one block (<= 128 registers): nothing left to relax
-        nxt = 12 if (regs <= 128 and "_2d_" in base) else 1
-        if nxt == cap or "_t32x" in base:
+        # next register budget (minimum resident blocks): 2D one-warp blocks 16 -> 12 -> 1
+        # (128 -> 168 -> 255 registers), two-warp blocks 8 -> 6 -> 3, 3D 2 -> 1.  A 512-thread 3D
+        # layout is already at one block (<= 128 registers): nothing left to relax
+        if "_w2" in base:
+            ladder = [6, 3]
+        elif "_2d_" in base:
+            ladder = [12, 1]
+        else:
+            ladder = [1]
+        nxt = next((c for c in ladder if regs < {12: 168, 1: 255, 6: 168, 3: 255}[c]), None)
+        if nxt is None or nxt == cap or "_t32x" in base:
             break
         cap = nxt
     if not known:
@@ -288,5 +307,25 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
     return LIB
 
 
+def update_caps():
+    """Record the cap each built instance ended with (its ptxas log) in regcaps.json."""
+    path = os.path.join(HERE, "regcaps.json")
+    with open(path) as f:
+        d = json.load(f)
+    for inst in instances():
+        name = inst_name(*inst)
+        log = os.path.join(OBJ, name + ".o.ptxas.log")
+        if name in d["caps"] or not os.path.exists(log):
+            continue
+        caps = re.findall(r"# AN5D_MINB_CAP=(\S+)", open(log).read())
+        d["caps"][name] = None if not caps or caps[-1] == "None" else int(caps[-1])
+    d["caps"] = dict(sorted(d["caps"].items()))
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1)
+
+
 if __name__ == "__main__":
-    build()
+    if "--update-caps" in sys.argv:
+        update_caps()
+    else:
+        build()

@@ -128,8 +128,13 @@ int cfg_tile_x(const Plan& p, const an5d_config& c) {
     return bs - 2 * hl + 2 * ((hl + A - 1) / A) * A;
 }
 
-const Instance* find_instance(const Plan& p, int bT, const an5d_config& c) {
-    return find_instance(p, bT, c.vec, c.direct, cfg_tile_x(p, c), c.n_thr);
+// The instance a sweep of degree d runs under configuration c: the configuration's layout, or for
+// a reduced degree (d < b_T) without that layout (the 2D level split needs d >= 2) the same tile
+// with any thread count -- identical per-cell arithmetic, so the results are the same bits.
+const Instance* find_instance(const Plan& p, int d, const an5d_config& c) {
+    const Instance* i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), c.n_thr);
+    if (!i && d < c.bT) i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), 0);
+    return i;
 }
 
 int max_bT_for(const Plan& p, int vec) {
@@ -431,10 +436,11 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
         if (hint && hint->n_thr && inst.threads != hint->n_thr) continue;
         if (hint && cfg_tile_x(p, *hint) && inst.tile_x_loaded != cfg_tile_x(p, *hint)) continue;
         if (T > 0 && inst.bT > T) continue;
-        // every reduced degree the schedule may need must exist with the same layout
+        // every reduced degree the schedule may need must exist with the same tile
         bool ok = true;
         for (int d = 1; d < inst.bT && ok; ++d)
-            ok = find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, inst.threads) != nullptr;
+            ok = find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, inst.threads) != nullptr ||
+                 find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, 0) != nullptr;
         if (!ok) continue;
         std::vector<int64_t> hs;
         if (hint && hint->h) {
@@ -769,10 +775,10 @@ an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config
         return fail(AN5D_ERR_UNSUPPORTED,
                     "no kernel instance for ndim=%d rad=%d shape=%d dtype=%d bT=%d vec=%d bS=(%d,%d) n_thr=%d", p.ndim,
                     p.rad, p.shape, p.dtype, c.bT, c.vec, c.bS[0], c.bS[1], c.n_thr);
-    for (int d = 1; d < c.bT; ++d)
-        if (!find_instance(p, d, c.vec, c.direct, inst->tile_x_loaded, inst->threads))
-            return fail(AN5D_ERR_UNSUPPORTED, "no reduced-degree instance d=%d for vec %d", d, c.vec);
     c.n_thr = inst->threads;
+    for (int d = 1; d < c.bT; ++d)
+        if (!find_instance(p, d, c))
+            return fail(AN5D_ERR_UNSUPPORTED, "no reduced-degree instance d=%d for vec %d", d, c.vec);
     // logical tile b_S reported back
     SweepGeom g{};
     an5d_status s = sweep_geometry(p, *inst, dm, c.bT, c.h ? c.h : dm.E[0], 0, dm.E[0], p.rad, dm.E[0] - p.rad, g);

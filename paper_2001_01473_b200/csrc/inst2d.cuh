@@ -6,7 +6,7 @@
 
 namespace an5d {
 
-template <typename T, int R, int BT, int V, bool BOX, bool ASSOC>
+template <typename T, int R, int BT, int V, bool BOX, bool ASSOC, int NW = 1>
 cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, bool /*edge*/,
                      cudaStream_t st) {
     Coeffs2D<T, R> cf;
@@ -15,30 +15,30 @@ cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, b
         if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
         else cf.c[i] = c[i];
     }
-    constexpr size_t smem = smem_bytes_2d<T, R, BT, V, ASSOC>();
-    auto fn = &an5d_sweep2d<T, R, BT, V, BOX, ASSOC>;
+    constexpr size_t smem = smem_bytes_2d<T, R, BT, V, ASSOC, NW>();
+    auto fn = &an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (smem > 48 * 1024 && !attr_set) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    fn<<<(unsigned)blocks, 32, smem, st>>>(a, cf);
+    fn<<<(unsigned)blocks, 32 * NW, smem, st>>>(a, cf);
     return cudaGetLastError();
 }
 
-template <typename T, int R, int BT, int V, bool BOX, bool ASSOC = true>
+template <typename T, int R, int BT, int V, bool BOX, bool ASSOC = true, int NW = 1>
 Instance make_instance2d() {
     Instance i{};
     i.ndim = 2; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
     i.rad = R; i.bT = BT; i.vec = V; i.assoc = ASSOC ? 1 : 0;
-    i.launch2d = &launch2d<T, R, BT, V, BOX, ASSOC>;
+    i.launch2d = &launch2d<T, R, BT, V, BOX, ASSOC, NW>;
     i.launch3d = nullptr;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, ASSOC>);
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW>);
     i.fn_edge = i.fn_interior;
-    i.threads = 32;
+    i.threads = 32 * NW;
     i.tile_x_loaded = 32 * V;
     i.tile_y = 0;
-    i.smem_bytes = smem_bytes_2d<T, R, BT, V, ASSOC>();
+    i.smem_bytes = smem_bytes_2d<T, R, BT, V, ASSOC, NW>();
     return i;
 }
 

@@ -53,11 +53,11 @@ def small_ext(ndim, rad):
 
 def configs_for(an5d, st, ext, ndim, direct=0):
     """A spread of available (bT, vec, layout) configurations for this stencil, with short stream
-    blocks so several stream blocks (and interior + edge units) are exercised.  3D: the default
-    256-thread layout and the 512-thread layouts (n_thr = 512: 64-wide fp64 / 128-wide fp32
-    tiles) where they are built."""
+    blocks so several stream blocks (and interior + edge units) are exercised.  2D: one warp per
+    tile and the two-warp level split (n_thr = 64); 3D: the default 256-thread layout and the
+    512-thread layouts (n_thr = 512: 64-wide fp64 / 128-wide fp32 tiles) where they are built."""
     out = []
-    for n_thr in ((0,) if ndim == 2 else (256, 512)):
+    for n_thr in ((32, 64) if ndim == 2 and not direct else (0,) if ndim == 2 else (256, 512)):
         for vec in (1, 2, 4, 8):
             bts = []
             for bT in range(1, 11):
@@ -320,6 +320,9 @@ def test_tune_then_run(an5d, name, dtype):
     ("star2d1r", torch.float32, {"bT": 7, "h": 16, "vec": 8}),
     ("box2d2r", torch.float64, {"bT": 2, "h": 8, "vec": 4}),
     ("j2d5pt", torch.float32, {"bT": 4, "h": 8, "vec": 8}),
+    ("star2d1r", torch.float32, {"bT": 7, "h": 16, "vec": 8, "n_thr": 64}),
+    ("star2d2r", torch.float64, {"bT": 3, "h": 8, "vec": 4, "n_thr": 64}),
+    ("box2d1r", torch.float32, {"bT": 5, "h": 8, "vec": 8, "n_thr": 64}),
 ])
 def test_stream_block_runs(an5d, name, dtype, cfg, monkeypatch):
     """2D run schedule (an5d_host.cu build_runs_2d: x-edge singles, y-edge singles, one round of
@@ -434,3 +437,24 @@ def test_full_size_linear_field_exact(an5d, name):
     st.run(a, b, 1000, cfg)
     torch.cuda.synchronize()
     assert torch.equal(b, lin), (name, cfg, float((b - lin).abs().max()))
+
+
+@pytest.mark.parametrize("name,dtype,bT,vec", [("star2d1r", torch.float32, 7, 8), ("star2d1r", torch.float32, 8, 8),
+                                               ("star2d2r", torch.float32, 4, 8), ("box2d1r", torch.float32, 4, 8),
+                                               ("star2d1r", torch.float64, 7, 4), ("j2d5pt", torch.float32, 6, 8)])
+def test_level_split_bit_identical(an5d, name, dtype, bT, vec):
+    """The two-warp level split (n_thr = 64: warp 0 levels 1..b_T/2, warp 1 the rest, rows handed
+    over through a shared-memory queue) does exactly the one-warp kernel's per-cell arithmetic, so
+    its result is the same bits -- on a grid with interior and edge units, several stream blocks,
+    a reduced-degree sweep (degree 1 runs the one-warp instance) -- and matches the oracle."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = (157 + 2 * rad, 1500 + 2 * rad)
+    g = inputs.global_grid(91, ext)
+    T = 2 * bT + 1
+    one, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, {"bT": bT, "vec": vec, "h": 24, "n_thr": 32})
+    two, st = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, {"bT": bT, "vec": vec, "h": 24, "n_thr": 64})
+    assert st.plan_config(ext, T, {"bT": bT, "vec": vec, "h": 24, "n_thr": 64})["n_thr"] == 64
+    assert np.array_equal(one, two), (name, bT)
+    exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+    assert ring_equal(two, exp, rad)
+    assert rel_linf(two, exp, rad) <= TOL[dtype]

@@ -20,3 +20,14 @@ for what in "$@"; do
           python tools/sweeponly.py ${NCU_CASE:-star2d1r f32 7 45 8 6} > gpurun_out/${TAG}_ncu_full.log 2>&1 ;;
   esac
 done
+# extra modes (run after the fixed ones): TAG suite3d / suite2d -> default-planner suite lines
+for what in "$@"; do
+  case $what in
+    suite3d)
+      python bench.py --suite all3d --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_suite3d.jsonl 2>> gpurun_out/${TAG}_suite.err
+      python bench.py --suite all3d --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --nthr 256 > gpurun_out/${TAG}_suite3d_n256.jsonl 2>> gpurun_out/${TAG}_suite.err
+      python bench.py --suite all3d --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --nthr 512 > gpurun_out/${TAG}_suite3d_n512.jsonl 2>> gpurun_out/${TAG}_suite.err ;;
+    suite2d)
+      python bench.py --suite all2d,config4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_suite2d.jsonl 2>> gpurun_out/${TAG}_suite.err ;;
+  esac
+done
