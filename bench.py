@@ -33,7 +33,7 @@ WORKLOADS = {
     "star2d1r-f32-16384": ("star2d1r", "float32", 16384, 1000),
 }
 for _n in ("star2d1r", "star2d2r", "star2d3r", "star2d4r", "box2d1r", "box2d2r", "box2d3r", "box2d4r",
-           "j2d5pt", "j2d9pt"):
+           "j2d5pt", "j2d9pt", "j2d9pt-gol"):
     for _dt in ("f32", "f64"):
         WORKLOADS[f"{_n}-{_dt}-16384"] = (_n, "float32" if _dt == "f32" else "float64", 16384, 1000)
 for _n in ("star3d1r", "star3d2r", "star3d3r", "star3d4r", "box3d1r", "box3d2r", "box3d3r", "box3d4r",

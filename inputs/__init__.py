@@ -31,7 +31,7 @@ STAR, BOX = 0, 1
 
 # PAPER.md Table 2: stencil name -> (ndim, rad, shape, has_divisor)
 # j2d5pt = star2d1r taps / c0; j2d9pt = star2d2r taps / c0 ("2nd-order" P:641-642);
-# j3d27pt = box3d1r taps / c0.
+# j3d27pt = box3d1r taps / c0; j2d9pt-gol = box2d1r taps / c0.
 BENCHMARKS = {}
 for _r in range(1, 5):
     BENCHMARKS[f"star2d{_r}r"] = (2, _r, STAR, False)
@@ -41,6 +41,8 @@ for _r in range(1, 5):
 BENCHMARKS["j2d5pt"] = (2, 1, STAR, True)
 BENCHMARKS["j2d9pt"] = (2, 2, STAR, True)
 BENCHMARKS["j3d27pt"] = (3, 1, BOX, True)
+# j2d9pt-gol = box2d1r taps / c0 (Table 2, the "game of life"-shaped 9-point Jacobi)
+BENCHMARKS["j2d9pt-gol"] = (2, 1, BOX, True)
 
 
 def _fmix32(h):

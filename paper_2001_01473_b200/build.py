@@ -37,7 +37,7 @@ REPO = os.path.dirname(HERE)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v",
+    "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas", "-v", "-diag-suppress", "177,836",
     "-I", "include",
 ] + os.environ.get("AN5D_EXTRA_NVCC", "").split()   # nvcc runs with cwd = REPO (relative paths)
 

@@ -149,6 +149,12 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // slot period P would multiply an already huge loop body by P (compile time, I-cache), so the
     // slots are rotated instead: 2*rad moves per cell and step against >= 125 FMAs.
     constexpr bool ROT = BOX && R >= 2;
+    // R >= 3 box: the per-plane contributions run as a runtime loop (see the level body)
+#ifdef AN5D_RLOOP_MIN_R
+    constexpr bool RLOOP = ROT && R >= AN5D_RLOOP_MIN_R;
+#else
+    constexpr bool RLOOP = ROT && R >= 3;
+#endif
     constexpr int U = ROT ? 1 : P;          // unroll factor of the stream loop
     // level skew (traits): SK = 1 -> level L at step s consumes level L-1's plane of step s-1;
     // levels run top-down inside a step (a level reads its arrival slot before the level below
@@ -377,6 +383,61 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                     return c < 0 ? hl[t][c + R] : (c >= VX ? hh[t][c - VX] : LN::cell(rowref(yr), c));
                 };
                 // contributions of arriving plane q = s - (L-1) R to output planes p = q - dz
+                if constexpr (RLOOP) {
+                    // high-order box: a RUNTIME loop over the 2 rad + 1 output planes (the static
+                    // unroll is 5-12k instructions per plane: instruction-fetch bound, ncu
+                    // r02b_ncu_b3d4r_f32: 53 % "no instruction" stalls).  The target plane is
+                    // always slot 0; the slots rotate by one after each plane (P rotations = the
+                    // identity), recycled slots start at zero (no first-tap multiply), and the
+                    // taps of plane dz = R - j come from the parameter bank with a runtime offset.
+#pragma unroll 1
+                    for (int j = 0; j < P; ++j) {
+                        const E* cz = &cf.c[(2 * R - j) * W * W];
+                        auto tap_to = [&](E (&tgt)[VY][NE], const E c, int dy, int dx) {
+#pragma unroll
+                            for (int yy = 0; yy < VY; ++yy) {
+                                if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                                    for (int e = 0; e < NE; ++e) tgt[yy][e] = LN::fma(c, X(yy + dy, e + dx), tgt[yy][e]);
+                                } else if ((dx & 1) == 0) {
+#pragma unroll
+                                    for (int e = 0; e < NE; ++e) {
+                                        const int jj = 2 * e + dx;
+                                        const E q = (jj >= 0 && jj + 1 < VX) ? rowref(yy + dy)[jj >> 1]
+                                                                             : make_float2(X(yy + dy, jj), X(yy + dy, jj + 1));
+                                        tgt[yy][e] = LN::fma(c, q, tgt[yy][e]);
+                                    }
+                                } else {
+#pragma unroll
+                                    for (int e = 0; e < NE; ++e) {
+                                        tgt[yy][e].x = fmaf(c.x, X(yy + dy, 2 * e + dx), tgt[yy][e].x);
+                                        tgt[yy][e].y = fmaf(c.x, X(yy + dy, 2 * e + 1 + dx), tgt[yy][e].y);
+                                    }
+                                }
+                            }
+                        };
+#pragma unroll
+                        for (int dy = -R; dy <= R; ++dy)
+#pragma unroll
+                            for (int dx = -R; dx <= R; ++dx) tap_to(acc[L - 1][0], cz[(dy + R) * W + (dx + R)], dy, dx);
+                        // rotate the slots left by one: the next plane's target moves to slot 0
+                        E t0[VY][NE];
+#pragma unroll
+                        for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                            for (int e = 0; e < NE; ++e) t0[yy][e] = acc[L - 1][0][yy][e];
+#pragma unroll
+                        for (int jj = 0; jj + 1 < P; ++jj)
+#pragma unroll
+                            for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                                for (int e = 0; e < NE; ++e) acc[L - 1][jj][yy][e] = acc[L - 1][jj + 1][yy][e];
+#pragma unroll
+                        for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                            for (int e = 0; e < NE; ++e) acc[L - 1][P - 1][yy][e] = t0[yy][e];
+                    }
+                } else
                 static_for<0, 2 * R + 1>([&](auto dc) {
                     constexpr int dz = R - decltype(dc)::value;
                     constexpr int slot = ROT ? R - dz : pmod(k - (L - 1) * DL - dz, P);
@@ -483,6 +544,14 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                         for (int yy = 0; yy < VY; ++yy)
 #pragma unroll
                             for (int e = 0; e < NE; ++e) acc[l][j][yy][e] = acc[l][j + 1][yy][e];
+                if constexpr (RLOOP) {   // the recycled slot accumulates from zero (no first-tap multiply)
+#pragma unroll
+                    for (int l = 0; l < BT; ++l)
+#pragma unroll
+                        for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                            for (int e = 0; e < NE; ++e) acc[l][P - 1][yy][e] = E{};
+                }
             }
         });
     }
@@ -510,7 +579,7 @@ template <typename T, int VY, int R, bool BOX, int TXT> constexpr int min_blocks
 
 template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4>
 __global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
-an5d_sweep3d(const Sweep3DArgs a, const Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
+an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* const smem = reinterpret_cast<T*>(smem_raw);

@@ -20,8 +20,7 @@ TOL = {torch.float32: 1e-5, torch.float64: 1e-12}
 NP = {torch.float32: np.float32, torch.float64: np.float64}
 
 # interior size of the reduced grid (2D: n x n, 3D: n^3), T = 1000 (SURVEY.md §8(d) Policy sizes)
-CASES = {name: (2048 if name.endswith(("2d1r", "2d2r", "2d3r", "2d4r", "5pt", "9pt")) else 128)
-         for name in inputs.BENCHMARKS}
+CASES = {name: (2048 if spec[0] == 2 else 128) for name, spec in inputs.BENCHMARKS.items()}
 
 
 def rel_linf(got, exp, rad):

@@ -51,5 +51,6 @@ def test_benchmark_catalogue_matches_table2():
     for r in range(1, 5):
         for s in ("star2d", "box2d", "star3d", "box3d"):
             assert f"{s}{r}r" in names
-    assert {"j2d5pt", "j2d9pt", "j3d27pt"} <= names
+    assert {"j2d5pt", "j2d9pt", "j3d27pt", "j2d9pt-gol"} <= names
+    assert inputs.BENCHMARKS["j2d9pt-gol"] == (2, 1, inputs.BOX, True)   # 3x3 box / c_0
     assert inputs.BENCHMARKS["j2d9pt"][1] == 2   # "2nd-order"

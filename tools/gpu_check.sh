@@ -31,3 +31,13 @@ for what in "$@"; do
       python bench.py --suite all2d,config4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_suite2d.jsonl 2>> gpurun_out/${TAG}_suite.err ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    split2d)
+      for w in star2d1r-f32-16384 star2d1r-f64-16384 star2d2r-f32-16384 star2d2r-f64-16384 box2d1r-f32-16384 j2d5pt-f32-16384 j2d9pt-f32-16384; do
+        for n in 32 64; do
+          python bench.py --workload $w --nthr $n --steps 3 --warmup 2 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_split2d.jsonl 2>> gpurun_out/${TAG}_suite.err
+        done
+      done ;;
+  esac
+done
