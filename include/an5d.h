@@ -150,6 +150,47 @@ an5d_status an5d_sweep(an5d_plan* plan, const void* src, void* dst, const int64_
                        int64_t outer_offset, int64_t global_outer_extent, int64_t out_lo,
                        int64_t out_hi, int32_t* debug_write_count, void* cuda_stream);
 
+/* ---- Fused halo exchange (slab mode on several GPUs) --------------
+ * A sweep of a slab can store its outermost output planes -- the planes the neighbouring slabs
+ * hold as ghost planes -- straight into the NEIGHBOURS' destination buffers, from the same
+ * kernel that computes them (the thread that stores a plane also stores it to the peer), so no
+ * separate exchange step exists.  The buffers are peer-mapped: another GPU's memory opened with
+ * an5d_ipc_open (NVLink P2P through NVSwitch), or another buffer on the same GPU.  Ordering
+ * between the slabs is stream-ordered with 32-bit flags (an5d_stream_signal / an5d_stream_wait):
+ * before sweep i every rank waits until its neighbours have finished sweep i-1 (their ghost
+ * stores into its src are complete, and they no longer read the buffer this sweep writes into). */
+typedef struct {
+    void* peer_dst[2];            /* [0] lower / [1] upper neighbour's buffer of the same parity as */
+                                  /* dst (device pointers valid on this device), or NULL           */
+    int64_t peer_plane_shift[2];  /* plane index in the neighbour's local array minus the plane    */
+                                  /* index here (= my outer_offset - the neighbour's outer_offset) */
+    int64_t send_planes[2];       /* the lowest [0] / highest [1] send_planes output planes of this */
+                                  /* sweep are also stored there (0 = none)                         */
+} an5d_peer_store;
+
+/* an5d_sweep with peer stores.  The neighbours' arrays must have this array's extents beyond the
+ * outermost dimension, the same pitches and the same alignment (checked: AN5D_ERR_UNSUPPORTED).
+ * peers == NULL is an5d_sweep.                                                                 */
+an5d_status an5d_sweep_peer(an5d_plan* plan, const void* src, void* dst, const int64_t* extents,
+                            const int64_t* pitches, int degree, const an5d_config* cfg,
+                            int64_t outer_offset, int64_t global_outer_extent, int64_t out_lo,
+                            int64_t out_hi, const an5d_peer_store* peers, int32_t* debug_write_count,
+                            void* cuda_stream);
+
+/* Stream-ordered flag write (after all prior work on the stream, with a memory barrier: the
+ * stream's earlier stores -- peer stores included -- are visible before the flag) and wait
+ * (the stream blocks until *flag >= value).  flag: a device pointer (own or peer-mapped).      */
+an5d_status an5d_stream_signal(uint32_t* flag, uint32_t value, void* cuda_stream);
+an5d_status an5d_stream_wait(const uint32_t* flag, uint32_t value, void* cuda_stream);
+
+/* CUDA IPC of a device allocation (one process per GPU): an5d_ipc_export writes the 64-byte
+ * handle of the allocation containing ptr and ptr's byte offset in it; an5d_ipc_open maps a
+ * handle from another process (peer access enabled lazily) and returns the allocation's base
+ * (add the offset); an5d_ipc_close unmaps it.                                                 */
+an5d_status an5d_ipc_export(const void* ptr, void* handle64, int64_t* offset);
+an5d_status an5d_ipc_open(const void* handle64, void** base);
+an5d_status an5d_ipc_close(void* base);
+
 /* Copy the rad-wide ring cells of src into dst (O(surface) kernel).  With outer_offset /
  * global_outer_extent as in an5d_sweep, only global ring planes/rows/columns are copied.       */
 an5d_status an5d_copy_ring(an5d_plan* plan, const void* src, void* dst, const int64_t* extents,
@@ -163,7 +204,8 @@ an5d_status an5d_plan_config(an5d_plan* plan, const int64_t* extents, int64_t T,
 
 /* Tuned configuration (the paper's procedure): rank every configuration with the
  * model of an5d_plan_config, run the best stream-block length of each of the top_k distinct
- * (bT, vec) pairs on the device and return the fastest (measured over two sweeps after a warm-up
+ * (bT, vec, layout) configurations -- plus the best one of every kernel layout the top_k missed --
+ * on the device and return the fastest (measured over two sweeps after a warm-up
  * sweep).  Non-zero fields of `hint` are kept, as in an5d_plan_config.
  *   grid_in: read only.  grid_out: overwritten (interior) -- pass the buffers of the following
  *   an5d_run, which rewrites grid_out entirely.  Same extents/pitches/alignment rules as an5d_run.

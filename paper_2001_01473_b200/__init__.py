@@ -61,6 +61,11 @@ class Geometry(ctypes.Structure):
         return out
 
 
+class PeerStore(ctypes.Structure):
+    _fields_ = [("peer_dst", ctypes.c_void_p * 2), ("peer_plane_shift", ctypes.c_int64 * 2),
+                ("send_planes", ctypes.c_int64 * 2)]
+
+
 class DeviceParams(ctypes.Structure):
     _fields_ = [("n_sm", ctypes.c_int), ("max_threads_per_sm", ctypes.c_int), ("peak_comp_gflops", ctypes.c_double),
                 ("peak_gm_gbs", ctypes.c_double), ("peak_sm_gbs", ctypes.c_double)]
@@ -92,6 +97,13 @@ def _load():
         "an5d_run": (I32, [P, P, P, pi64, pi64, I64, ctypes.POINTER(Config), P]),
         "an5d_sweep": (I32, [P, P, P, pi64, pi64, I32, ctypes.POINTER(Config), I64, I64, I64, I64, P, P]),
         "an5d_copy_ring": (I32, [P, P, P, pi64, pi64, I64, I64, P]),
+        "an5d_sweep_peer": (I32, [P, P, P, pi64, pi64, I32, ctypes.POINTER(Config), I64, I64, I64, I64,
+                                  ctypes.POINTER(PeerStore), P, P]),
+        "an5d_stream_signal": (I32, [P, ctypes.c_uint32, P]),
+        "an5d_stream_wait": (I32, [P, ctypes.c_uint32, P]),
+        "an5d_ipc_export": (I32, [P, P, pi64]),
+        "an5d_ipc_open": (I32, [P, ctypes.POINTER(P)]),
+        "an5d_ipc_close": (I32, [P]),
         "an5d_plan_config": (I32, [P, pi64, I64, ctypes.POINTER(Config), ctypes.POINTER(Config)]),
         "an5d_describe": (I32, [P, pi64, ctypes.POINTER(Config), ctypes.POINTER(Geometry)]),
         "an5d_tune": (I32, [P, P, P, pi64, pi64, I64, ctypes.POINTER(Config), I32, ctypes.POINTER(Config),
@@ -137,7 +149,8 @@ def load():
 def loaded() -> bool:
     return _LazyLib._h is not None
 
-EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
+EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_stream_signal",
+                    "an5d_stream_wait", "an5d_ipc_export", "an5d_ipc_open", "an5d_ipc_close", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
                     "an5d_describe", "an5d_schedule", "an5d_model_paper", "an5d_model_paper_search",
                     "an5d_last_launch_count", "an5d_destroy", "an5d_last_error", "an5d_version")
 
@@ -296,8 +309,10 @@ class Stencil:
 
     def sweep(self, src: torch.Tensor, dst: torch.Tensor, degree: int, cfg, outer_offset: int = 0,
               global_outer_extent: int | None = None, out_lo: int | None = None, out_hi: int | None = None,
-              write_count: torch.Tensor | None = None, stream=None):
-        """One sweep of `degree` time steps (slab mode; see an5d.h an5d_sweep)."""
+              write_count: torch.Tensor | None = None, stream=None, peers=None):
+        """One sweep of `degree` time steps (slab mode; see an5d.h an5d_sweep).  ``peers``: None or
+        a dict {"lo"/"hi": (device pointer int, plane shift, planes)} for the fused halo exchange
+        (an5d_sweep_peer)."""
         ext, pit = _geom_of(src)
         g = ext[0] if global_outer_extent is None else global_outer_extent
         lo = self.rad if out_lo is None else out_lo
@@ -305,6 +320,18 @@ class Stencil:
         st = stream if stream is not None else torch.cuda.current_stream(src.device)
         c = _cfg(cfg)
         wc = write_count.data_ptr() if write_count is not None else None
+        if peers:
+            ps = PeerStore()
+            for k, side in enumerate(("lo", "hi")):
+                if side in peers and peers[side]:
+                    ptr, shift, n = peers[side]
+                    ps.peer_dst[k] = int(ptr)
+                    ps.peer_plane_shift[k] = int(shift)
+                    ps.send_planes[k] = int(n)
+            _check(_lib.an5d_sweep_peer(self._h, src.data_ptr(), dst.data_ptr(), _i64(ext), _i64(pit), int(degree),
+                                        ctypes.byref(c), int(outer_offset), int(g), int(lo), int(hi), ctypes.byref(ps),
+                                        wc, ctypes.c_void_p(st.cuda_stream)))
+            return
         _check(_lib.an5d_sweep(self._h, src.data_ptr(), dst.data_ptr(), _i64(ext), _i64(pit), int(degree),
                                ctypes.byref(c), int(outer_offset), int(g), int(lo), int(hi), wc,
                                ctypes.c_void_p(st.cuda_stream)))
@@ -350,6 +377,37 @@ class Stencil:
 
     def last_launch_count(self) -> int:
         return int(_lib.an5d_last_launch_count(self._h))
+
+
+def stream_signal(flag_ptr: int, value: int, stream=None):
+    """Stream-ordered write of a 32-bit device flag after the stream's prior work (an5d.h)."""
+    st = stream if stream is not None else torch.cuda.current_stream()
+    _check(_lib.an5d_stream_signal(ctypes.c_void_p(int(flag_ptr)), int(value), ctypes.c_void_p(st.cuda_stream)))
+
+
+def stream_wait(flag_ptr: int, value: int, stream=None):
+    """The stream waits until the 32-bit device flag is >= value (an5d.h)."""
+    st = stream if stream is not None else torch.cuda.current_stream()
+    _check(_lib.an5d_stream_wait(ctypes.c_void_p(int(flag_ptr)), int(value), ctypes.c_void_p(st.cuda_stream)))
+
+
+def ipc_export(ptr: int):
+    """(64-byte handle, byte offset) of the allocation holding a device pointer (CUDA IPC)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _check(_lib.an5d_ipc_export(ctypes.c_void_p(int(ptr)), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation (CUDA IPC); returns its base device pointer here."""
+    base = ctypes.c_void_p()
+    _check(_lib.an5d_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(base)))
+    return int(base.value)
+
+
+def ipc_close(base: int):
+    _check(_lib.an5d_ipc_close(ctypes.c_void_p(int(base))))
 
 
 def version() -> str:

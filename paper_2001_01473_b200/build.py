@@ -73,10 +73,11 @@ LAYOUTS = {"": (16, 4), "t32x2": (32, 2), "t32x4": (32, 4)}   # 3D layout -> (TX
 # 2D level split "w2" (kernel2d.cuh Split2D): two warps per tile, warp 0 levels 1..b_T/2 with the
 # staging, warp 1 the rest with the store -- half the partial-sum registers per warp.  b_T 1 has
 # nothing to split: the reduced-degree sweep of degree 1 uses the one-warp instance.
-CORE_SPLIT = {
-    (2, 0, 0, 1): [(8, 10)], (2, 0, 0, 2): [(8, 6)], (2, 0, 1, 1): [(8, 6)],
-    (2, 1, 0, 1): [(4, 8)], (2, 1, 0, 2): [(4, 5)],
-}
+# Measured on B200 (profiles/r02d_split2d.jsonl): 8-13 % SLOWER than one warp per tile for
+# every stencil tried, so the default build keeps only star2d1r (tests, bench --nthr 64) and the
+# full build the rest.
+CORE_SPLIT = {(2, 0, 0, 1): [(8, 8)], (2, 1, 0, 1): [(4, 7)]}
+FULL_SPLIT = {(2, 0, 0, 2): [(8, 6)], (2, 0, 1, 1): [(8, 6)], (2, 1, 0, 2): [(4, 5)]}
 
 
 def full_instances():
@@ -132,7 +133,9 @@ def instances():
     full b_T-sweep matrix (plus the core set); AN5D_DEV_INSTANCES: a development subset."""
     out = core_instances()
     if os.environ.get("AN5D_FULL_BUILD", "") not in ("", "0"):
-        out = sorted(set(out) | set(full_instances()))
+        extra = [(nd, dt, sh, r, bT, v, 1, "w2") for (nd, dt, sh, r), lst in FULL_SPLIT.items()
+                 for v, bmax in lst for bT in range(2, bmax + 1)]
+        out = sorted(set(out) | set(full_instances()) | set(extra))
     dev = os.environ.get("AN5D_DEV_INSTANCES")
     if dev:
         # quick development subset: comma list of "ndim:dtype:shape:rad" groups, or "min"

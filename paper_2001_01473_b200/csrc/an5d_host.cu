@@ -11,6 +11,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/an5d.h"
@@ -609,8 +610,30 @@ an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src,
 }
 
 // One sweep: edge units on the side stream, interior units on the caller's stream, joined.
+// Peer-store fields of a sweep's argument block (fused halo exchange): element shifts from the
+// per-plane strides.  Planes [out_lo, out_lo + n0) also go to the lower neighbour, [out_hi - n1,
+// out_hi) to the upper one.
+template <typename Args>
+void set_peers(Args& a, const an5d_peer_store* ps, int64_t plane_stride, int64_t out_lo, int64_t out_hi) {
+    a.peer_lo = a.peer_hi = nullptr;
+    a.send_lo_end = out_lo;
+    a.send_hi_begin = out_hi;
+    if (!ps) return;
+    if (ps->peer_dst[0] && ps->send_planes[0] > 0) {
+        a.peer_lo = ps->peer_dst[0];
+        a.peer_lo_shift = ps->peer_plane_shift[0] * plane_stride;
+        a.send_lo_end = out_lo + ps->send_planes[0];
+    }
+    if (ps->peer_dst[1] && ps->send_planes[1] > 0) {
+        a.peer_hi = ps->peer_dst[1];
+        a.peer_hi_shift = ps->peer_plane_shift[1] * plane_stride;
+        a.send_hi_begin = out_hi - ps->send_planes[1];
+    }
+}
+
 an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, int d, const an5d_config& cfg,
                          int64_t g_off, int64_t gE0, int64_t out_lo, int64_t out_hi, int32_t* wc,
+                         const an5d_peer_store* peers,
                          cudaStream_t st) {
     const Instance* inst = find_instance(p, d, cfg);
     if (!inst) return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for degree %d vec %d", d, cfg.vec);
@@ -626,6 +649,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.h = g.h; a.n_units = g.n_units; a.n_sb = g.n_sb;
         a.ctr = p.ctr + 2 * (p.ctr_seq++ % kCtrRing);
         a.wc = wc; a.Ex = (int)dm.E[1]; a.C = g.C[0]; a.H = g.halo[0]; a.n_tiles_x = (int)g.ntiles[0];
+        set_peers(a, peers, dm.pitch[0], out_lo, out_hi);
         const int64_t cap = (int64_t)resident_blocks(*inst) * dev_info().n_sm;
         const int64_t blocks = std::min<int64_t>(g.n_units, cap);
         const double frac = run_frac();
@@ -678,6 +702,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.src = src; a.dst = dst; a.pz = dm.pitch[0]; a.py = dm.pitch[1];
         a.Ez = dm.E[0]; a.g_off = g_off; a.gEz = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
         a.h = g.h; a.n_sb = g.n_sb; a.n_units = g.n_units; a.wc = wc;
+        set_peers(a, peers, dm.pitch[0], out_lo, out_hi);
         const double frac = run_frac();
         if (frac > 0) {
             const int64_t W = run_warps((int64_t)resident_blocks(*inst) * dev_info().n_sm);
@@ -849,6 +874,21 @@ std::vector<T> fold_coefficients(const double* c, size_t n, double divisor) {
 
 using namespace an5d;
 
+namespace {
+typedef CUresult (*StreamValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*AddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+template <typename F>
+F driver_fn(const char* name) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return reinterpret_cast<F>(f);
+}
+}  // namespace
+
 // =============================================================================================
 // C ABI
 // =============================================================================================
@@ -977,6 +1017,17 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             if (!seen) cand.push_back(r.second);
             if ((int)cand.size() >= top_k) break;
         }
+        // ... plus the model's best configuration of every kernel layout (vec, threads, tile
+        // width) the top k missed: the model ranks layouts only roughly (measured on B200: the
+        // 512-thread fp64 3D layout is 15-30 % faster, but its model rank varies by stencil)
+        auto layout_of = [&](const an5d_config& c) {
+            return std::make_tuple(c.vec, c.n_thr, cfg_tile_x(*p, c));
+        };
+        for (const auto& r : ranked) {
+            bool have = false;
+            for (const auto& c : cand) have = have || layout_of(c) == layout_of(r.second);
+            if (!have) cand.push_back(r.second);
+        }
         if (cand.empty())
             return fail(AN5D_ERR_UNSUPPORTED, "no feasible kernel instance for ndim=%d rad=%d shape=%d dtype=%d",
                         p->ndim, p->rad, p->shape, p->dtype);
@@ -996,11 +1047,11 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         auto measure = [&](const an5d_config& c0, an5d_config& c) -> double {
             if (resolve_config(*p, dm, T, &c0, c) != AN5D_OK) return 1e300;
             bool ok = launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
-                                   nullptr, st) == AN5D_OK;
+                                   nullptr, nullptr, st) == AN5D_OK;
             cudaEventRecord(e0, st);
             for (int r = 0; r < 2 && ok; ++r)
                 ok = launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
-                                  nullptr, st) == AN5D_OK;
+                                  nullptr, nullptr, st) == AN5D_OK;
             cudaEventRecord(e1, st);
             if (cudaEventSynchronize(e1) != cudaSuccess || !ok) {
                 cudaGetLastError();
@@ -1111,9 +1162,10 @@ an5d_status an5d_copy_ring(an5d_plan* p, const void* src, void* dst, const int64
     }
 }
 
-an5d_status an5d_sweep(an5d_plan* p, const void* src, void* dst, const int64_t* extents, const int64_t* pitches,
-                       int degree, const an5d_config* cfg, int64_t outer_offset, int64_t global_outer_extent,
-                       int64_t out_lo, int64_t out_hi, int32_t* debug_write_count, void* stream) {
+an5d_status an5d_sweep_peer(an5d_plan* p, const void* src, void* dst, const int64_t* extents, const int64_t* pitches,
+                            int degree, const an5d_config* cfg, int64_t outer_offset, int64_t global_outer_extent,
+                            int64_t out_lo, int64_t out_hi, const an5d_peer_store* peers, int32_t* debug_write_count,
+                            void* stream) {
     try {
         if (!p || !cfg) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
         Dims dm{};
@@ -1134,14 +1186,75 @@ an5d_status an5d_sweep(an5d_plan* p, const void* src, void* dst, const int64_t* 
             return fail(AN5D_ERR_INVALID_ARGUMENT, "slab lacks %d ghost planes below", degree * p->rad);
         if (out_hi + (int64_t)degree * p->rad > dm.E[0] && outer_offset + dm.E[0] < global_outer_extent)
             return fail(AN5D_ERR_INVALID_ARGUMENT, "slab lacks %d ghost planes above", degree * p->rad);
+        if (peers) {
+            for (int k = 0; k < 2; ++k) {
+                if (peers->send_planes[k] < 0 || peers->send_planes[k] > out_hi - out_lo)
+                    return fail(AN5D_ERR_INVALID_ARGUMENT, "send_planes[%d] outside the output planes", k);
+                if (peers->peer_dst[k] && check_alignment(*p, peers->peer_dst[k], dm, "peer_dst") != AN5D_OK)
+                    return AN5D_ERR_UNSUPPORTED;
+            }
+        }
         an5d_config c{};
         if ((s = resolve_config(*p, dm, 0, cfg, c)) != AN5D_OK) return s;
         if ((s = ensure_streams(*p)) != AN5D_OK) return s;
         return launch_sweep(*p, src, dst, dm, degree, c, outer_offset, global_outer_extent, out_lo, out_hi,
-                            debug_write_count, (cudaStream_t)stream);
+                            debug_write_count, peers, (cudaStream_t)stream);
     } catch (...) {
         return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
     }
+}
+
+an5d_status an5d_sweep(an5d_plan* p, const void* src, void* dst, const int64_t* extents, const int64_t* pitches,
+                       int degree, const an5d_config* cfg, int64_t outer_offset, int64_t global_outer_extent,
+                       int64_t out_lo, int64_t out_hi, int32_t* debug_write_count, void* stream) {
+    return an5d_sweep_peer(p, src, dst, extents, pitches, degree, cfg, outer_offset, global_outer_extent, out_lo,
+                           out_hi, nullptr, debug_write_count, stream);
+}
+
+// ---- stream-ordered flags and CUDA IPC (fused multi-GPU halo exchange plumbing) -----------------
+
+an5d_status an5d_stream_signal(uint32_t* flag, uint32_t value, void* stream) {
+    static StreamValue32Fn fn = driver_fn<StreamValue32Fn>("cuStreamWriteValue32");
+    if (!flag) return fail(AN5D_ERR_INVALID_ARGUMENT, "flag is NULL");
+    if (!fn) return fail(AN5D_ERR_CUDA, "cuStreamWriteValue32 not available");
+    const CUresult r = fn((CUstream)stream, (CUdeviceptr)flag, value, 0 /* with a memory barrier */);
+    return r == CUDA_SUCCESS ? AN5D_OK : fail(AN5D_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+}
+
+an5d_status an5d_stream_wait(const uint32_t* flag, uint32_t value, void* stream) {
+    static StreamValue32Fn fn = driver_fn<StreamValue32Fn>("cuStreamWaitValue32");
+    if (!flag) return fail(AN5D_ERR_INVALID_ARGUMENT, "flag is NULL");
+    if (!fn) return fail(AN5D_ERR_CUDA, "cuStreamWaitValue32 not available");
+    const CUresult r = fn((CUstream)stream, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
+    return r == CUDA_SUCCESS ? AN5D_OK : fail(AN5D_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}
+
+an5d_status an5d_ipc_export(const void* ptr, void* handle, int64_t* offset) {
+    static AddressRangeFn range = driver_fn<AddressRangeFn>("cuMemGetAddressRange");
+    if (!ptr || !handle || !offset) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!range) return fail(AN5D_ERR_CUDA, "cuMemGetAddressRange not available");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return fail(AN5D_ERR_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    memcpy(handle, &h, sizeof h);
+    *offset = (int64_t)((CUdeviceptr)ptr - base);
+    return AN5D_OK;
+}
+
+an5d_status an5d_ipc_open(const void* handle, void** base) {
+    if (!handle || !base) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    const cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? AN5D_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+an5d_status an5d_ipc_close(void* base) {
+    const cudaError_t e = cudaIpcCloseMemHandle(base);
+    return e == cudaSuccess ? AN5D_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
 an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t* extents, const int64_t* pitches,
@@ -1177,7 +1290,8 @@ an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t*
         for (size_t i = 0; i < deg.size(); ++i) {
             const void* src = bufs[i % 2];
             void* dst = bufs[(i + 1) % 2];
-            if ((s = launch_sweep(*p, src, dst, dm, deg[i], c, 0, dm.E[0], p->rad, dm.E[0] - p->rad, nullptr, st)) !=
+            if ((s = launch_sweep(*p, src, dst, dm, deg[i], c, 0, dm.E[0], p->rad, dm.E[0] - p->rad, nullptr, nullptr,
+                                  st)) !=
                 AN5D_OK)
                 return s;
         }

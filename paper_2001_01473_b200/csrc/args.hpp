@@ -23,6 +23,13 @@ struct Sweep2DArgs {
     long long* unit_ns;   // debug: per-unit (start, end, smid) globaltimer stamps, or nullptr
     const int4* runs;     // unit -> {tile_x, first stream block, end stream block}, or nullptr
                           // (then unit = one stream block in the fixed edge-first order)
+    // fused halo exchange (NEXT N1): output rows [out_lo, send_lo_end) are also stored into
+    // peer_lo at element offset (local offset + peer_lo_shift), rows [send_hi_begin, out_hi) into
+    // peer_hi -- the neighbours' ghost rows, peer-mapped (NVLink P2P / CUDA IPC); nullptr = none
+    void* peer_lo;
+    void* peer_hi;
+    int64_t peer_lo_shift, peer_hi_shift;
+    int64_t send_lo_end, send_hi_begin;
     int Ex;               // x extent (ring included)
     int C;                // compute width per tile (aligned to 16 bytes)
     int H;                // loaded halo per side (>= degree*rad, multiple of the vector width)
@@ -42,6 +49,10 @@ struct Sweep3DArgs {
     int32_t* wc;             // debug store counts (dense Ez x Ey x Ex) or nullptr
     const int4* runs;        // unit -> {tile y, tile x, first stream block, end stream block}, or
                              // nullptr (then unit = one stream block in the fixed frame-first order)
+    void* peer_lo;           // fused halo exchange: as Sweep2DArgs (planes instead of rows)
+    void* peer_hi;
+    int64_t peer_lo_shift, peer_hi_shift;
+    int64_t send_lo_end, send_hi_begin;
     int Ey, Ex;
     int Cy, Cx;              // compute region per tile
     int Hy, Hx;              // loaded halo per side (Hy = degree*rad; Hx rounded to 16 bytes)

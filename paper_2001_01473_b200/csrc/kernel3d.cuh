@@ -149,11 +149,14 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // slot period P would multiply an already huge loop body by P (compile time, I-cache), so the
     // slots are rotated instead: 2*rad moves per cell and step against >= 125 FMAs.
     constexpr bool ROT = BOX && R >= 2;
-    // R >= 3 box: the per-plane contributions run as a runtime loop (see the level body)
+    // fp32 box rad 4 (729 taps): the per-plane contributions run as a runtime loop (see the level
+    // body).  Measured on B200 (profiles/r02d_boxhi.jsonl): box3d4r fp32 12.2 -> 18.3 GCells/s;
+    // box3d3r fp32 -9 %, fp64 box3d3r -14 % and box3d4r -55 % (the rotation spills at 255
+    // registers), so those keep the static unroll.
 #ifdef AN5D_RLOOP_MIN_R
     constexpr bool RLOOP = ROT && R >= AN5D_RLOOP_MIN_R;
 #else
-    constexpr bool RLOOP = ROT && R >= 3;
+    constexpr bool RLOOP = ROT && R >= 4 && sizeof(T) == 4;
 #endif
     constexpr int U = ROT ? 1 : P;          // unroll factor of the stream loop
     // level skew (traits): SK = 1 -> level L at step s consumes level L-1's plane of step s-1;
@@ -508,20 +511,29 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             if (pi >= rp0 && pi < rp1) {
                 const int64_t p = s - (int64_t)(BT - 1) * DL - R;
                 const auto& fin = acc[BT - 1][ROT ? 0 : pmod(k - (BT - 1) * DL - R, P)];
-                T* op = dst + st_off;
+                auto put = [&](T* op) {
 #pragma unroll
-                for (int yy = 0; yy < VY; ++yy) {
-                    T c[VX];
-                    LN::to_cells(c, fin[yy]);
+                    for (int yy = 0; yy < VY; ++yy) {
+                        T c[VX];
+                        LN::to_cells(c, fin[yy]);
 #pragma unroll
-                    for (int j = 0; j < NCH; ++j) {
-                        if ((st_full >> (yy * NCH + j)) & 1u) st_vec_global<T>(op + yy * a.py + j * A, c + j * A);
-                        if constexpr (EDGE) {
+                        for (int j = 0; j < NCH; ++j) {
+                            if ((st_full >> (yy * NCH + j)) & 1u) st_vec_global<T>(op + yy * a.py + j * A, c + j * A);
+                            if constexpr (EDGE) {
 #pragma unroll
-                            for (int e = 0; e < A; ++e)
-                                if ((st_elem >> (yy * VX + j * A + e)) & 1u) op[yy * a.py + j * A + e] = c[j * A + e];
+                                for (int e = 0; e < A; ++e)
+                                    if ((st_elem >> (yy * VX + j * A + e)) & 1u) op[yy * a.py + j * A + e] = c[j * A + e];
+                            }
                         }
                     }
+                };
+                put(dst + st_off);
+                // fused halo exchange: the neighbours' ghost planes, stored straight into their
+                // (peer-mapped) buffers by the same thread (NEXT N1)
+                if (a.peer_lo && p < a.send_lo_end) put(static_cast<T*>(a.peer_lo) + (st_off + a.peer_lo_shift));
+                if (a.peer_hi && p >= a.send_hi_begin) put(static_cast<T*>(a.peer_hi) + (st_off + a.peer_hi_shift));
+#pragma unroll
+                for (int yy = 0; yy < VY; ++yy) {
                     if (a.wc) {
                         const int y = gy0 + yy;
 #pragma unroll

@@ -82,6 +82,21 @@ def partition(gE0: int, rad: int, nranks: int, G: int, align: int = 1):
     return out
 
 
+def partition_aligned(gE0: int, rad: int, nranks: int, G: int, h: int):
+    """:func:`partition` with owned chunks a multiple of the stream-block length h (SURVEY.md
+    §8(e): slab boundaries then fall on stream-block boundaries, so slabs add no stream-block
+    overlap beyond the single-GPU one), falling back to unaligned chunks when aligning would leave
+    a rank with fewer than G planes."""
+    if h > 1:
+        try:
+            parts = partition(gE0, rad, nranks, G, align=h)
+            if all(p.own_hi - p.own_lo >= max(1, G if nranks > 1 else 1) for p in parts):
+                return parts
+        except ValueError:
+            pass
+    return partition(gE0, rad, nranks, G, align=1)
+
+
 @dataclasses.dataclass(frozen=True)
 class SweepParts:
     """Output-plane ranges (local coordinates) of one sweep on one slab."""
@@ -225,6 +240,128 @@ def run_loopback(stencil, slabs, bufs_per_slab, T: int, cfg: dict, schedule_fn=N
 
 
 # ---------------------------------------------------------------------------------------------
+# Fused halo exchange: the boundary planes are stored into the
+# neighbours' ghost planes by the sweep kernel itself (an5d_sweep_peer); stream-ordered flags
+# order the slabs.  No separate exchange step, no NCCL on the data path.
+# ---------------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class PeerLink:
+    """One neighbour as seen from this rank: its two slab buffers (device pointers valid on this
+    device, same parity order as ours), its plane shift (our loc_lo - its loc_lo) and its
+    progress flag (uint32 device pointer)."""
+    bufs: tuple
+    shift: int
+    flag: int
+
+
+@dataclasses.dataclass
+class FusedLinks:
+    lo: PeerLink | None
+    hi: PeerLink | None
+    flag: int          # this rank's progress flag (uint32 device pointer)
+    epoch: int = 0     # sweeps completed by every rank in earlier runs (flags are never reset)
+
+
+def run_fused(stencil, s: Slab, bufs, T: int, cfg: dict, links: FusedLinks, stream=None, schedule_fn=None):
+    """One rank's share of a T-step run with the fused halo exchange.  Before sweep i a rank waits
+    until both neighbours finished sweep i-1 (flag >= epoch + i): its ghost planes for sweep i are
+    then stored, and the neighbours no longer read the buffer sweep i writes ghosts into.  Sweep i
+    stores the d_next * rad outermost owned planes into the neighbours' buffers of the same parity
+    as its destination; then the rank signals flag = epoch + i + 1.  Returns grid_out (bufs[1])."""
+    import paper_2001_01473_b200 as an5d
+    from . import schedule as lib_schedule
+    degrees, trailing = (schedule_fn or lib_schedule)(T, cfg["bT"])
+    a, b = bufs
+    st = stream
+    stencil.copy_ring(a, b, outer_offset=s.loc_lo, global_outer_extent=s.gE0, stream=st)
+    for i, d in enumerate(degrees):
+        src, dst = (a, b) if i % 2 == 0 else (b, a)
+        par = (i + 1) % 2                      # parity of dst: 1 = b, 0 = a
+        nd = degrees[i + 1] if i + 1 < len(degrees) else 0
+        g = nd * s.rad
+        for ln in (links.lo, links.hi):
+            if ln is not None:
+                an5d.stream_wait(ln.flag, links.epoch + i, st)
+        peers = {}
+        if links.lo is not None and g:
+            peers["lo"] = (links.lo.bufs[par], links.lo.shift, g)
+        if links.hi is not None and g:
+            peers["hi"] = (links.hi.bufs[par], links.hi.shift, g)
+        stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=s.gE0, out_lo=s.out_lo,
+                      out_hi=s.out_hi, stream=st, peers=peers or None)
+        an5d.stream_signal(links.flag, links.epoch + i + 1, st)
+    links.epoch += len(degrees)
+    if trailing:
+        n = s.out_hi - s.out_lo
+        import torch
+        with torch.cuda.stream(st) if st is not None else _nullctx():
+            _plane_view(b, s.out_lo, n).copy_(_plane_view(a, s.out_lo, n))
+    return b
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def loopback_fused(stencil, slabs, bufs_per_slab, T: int, cfg: dict, schedule_fn=None):
+    """All slabs on ONE device, one CUDA stream per slab, peer pointers = the other slabs'
+    buffers: the fused exchange's kernel-side peer stores and its flag protocol, with the slabs
+    genuinely running concurrently (single-GPU test of the multi-GPU data path)."""
+    import torch
+    dev = bufs_per_slab[0][0].device
+    n = len(slabs)
+    flags = torch.zeros(n * 32, dtype=torch.int32, device=dev)   # one flag per 128-byte line
+    fptr = lambda k: flags.data_ptr() + 128 * k
+    links = []
+    for k, s in enumerate(slabs):
+        lo = PeerLink(tuple(t.data_ptr() for t in bufs_per_slab[k - 1]), s.loc_lo - slabs[k - 1].loc_lo,
+                      fptr(k - 1)) if k > 0 else None
+        hi = PeerLink(tuple(t.data_ptr() for t in bufs_per_slab[k + 1]), s.loc_lo - slabs[k + 1].loc_lo,
+                      fptr(k + 1)) if k + 1 < n else None
+        links.append(FusedLinks(lo, hi, fptr(k)))
+    streams = [torch.cuda.Stream(dev) for _ in range(n)]
+    torch.cuda.synchronize(dev)
+    from . import schedule as lib_schedule
+    degrees, trailing = (schedule_fn or lib_schedule)(T, cfg["bT"])
+    # interleave the ranks sweep by sweep (host order only; the flags order the device work)
+    import paper_2001_01473_b200 as an5d
+    for k, s in enumerate(slabs):
+        a, b = bufs_per_slab[k]
+        stencil.copy_ring(a, b, outer_offset=s.loc_lo, global_outer_extent=s.gE0, stream=streams[k])
+    for i, d in enumerate(degrees):
+        nd = degrees[i + 1] if i + 1 < len(degrees) else 0
+        g = nd * slabs[0].rad
+        for k, s in enumerate(slabs):
+            a, b = bufs_per_slab[k]
+            src, dst = (a, b) if i % 2 == 0 else (b, a)
+            par = (i + 1) % 2
+            ln = links[k]
+            for peer in (ln.lo, ln.hi):
+                if peer is not None:
+                    an5d.stream_wait(peer.flag, i, streams[k])
+            peers = {}
+            if ln.lo is not None and g:
+                peers["lo"] = (ln.lo.bufs[par], ln.lo.shift, g)
+            if ln.hi is not None and g:
+                peers["hi"] = (ln.hi.bufs[par], ln.hi.shift, g)
+            stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=s.gE0, out_lo=s.out_lo,
+                          out_hi=s.out_hi, stream=streams[k], peers=peers or None)
+            an5d.stream_signal(ln.flag, i + 1, streams[k])
+    for k, s in enumerate(slabs):
+        if trailing:
+            a, b = bufs_per_slab[k]
+            m = s.out_hi - s.out_lo
+            with torch.cuda.stream(streams[k]):
+                _plane_view(b, s.out_lo, m).copy_(_plane_view(a, s.out_lo, m))
+    torch.cuda.synchronize(dev)
+    return [b for _, b in bufs_per_slab]
+
+
+# ---------------------------------------------------------------------------------------------
 # bench.py --gpus N (N > 1): one process per GPU under torchrun
 # ---------------------------------------------------------------------------------------------
 def bench_main(args, workloads):
@@ -251,7 +388,7 @@ def bench_main(args, workloads):
     st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
     # the planner picks (bT, vec, h) for this rank's slab shape
     probe = (-(-n // ws) + 2 * rad,) + gext[1:]
-    hint = {"bT": args.bt, "vec": args.vec, "h": args.h}
+    hint = {"bT": args.bt, "vec": args.vec, "h": args.h, "n_thr": getattr(args, "nthr", 0)}
     cfg = st.plan_config(probe, T, hint)
     tuned = False
     if not getattr(args, "no_tune", False):
@@ -264,13 +401,13 @@ def bench_main(args, workloads):
         obj = [None]
         if rank == 0:
             t = st.tune(pa, pb, T, hint, top_k=5)
-            obj = [{"bT": t["bT"], "vec": t["vec"], "h": t["h"]}]
+            obj = [{k: t[k] for k in ("bT", "vec", "h", "n_thr", "bS", "direct")}]
         dist.broadcast_object_list(obj, src=0)
         cfg = st.plan_config(probe, T, obj[0])
         tuned = True
         del pa, pb
         torch.cuda.synchronize()
-    slabs = partition(gext[0], rad, ws, cfg["bT"] * rad, align=1)
+    slabs = partition_aligned(gext[0], rad, ws, cfg["bT"] * rad, int(cfg["h"] or 1))
     s = slabs[rank]
     lext = local_extents(s, gext[1:])
     a = an5d.empty_grid(lext, rad, dtype, dev)

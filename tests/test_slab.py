@@ -31,6 +31,21 @@ def test_partition_covers_interior_disjointly():
         assert owned == list(range(rad, gE0 - rad))
 
 
+def test_partition_aligned_to_stream_blocks():
+    """Owned chunks are multiples of h where that leaves every rank >= G planes,
+    else the plain split; both cover the interior disjointly."""
+    for gE0, rad, n, G, h in [(1540, 2, 8, 6, 64), (1540, 2, 4, 6, 78), (518, 3, 4, 9, 100), (40, 1, 3, 4, 16)]:
+        parts = slab.partition_aligned(gE0, rad, n, G, h)
+        owned = []
+        for s in parts:
+            owned += list(range(s.own_lo, s.own_hi))
+        assert owned == list(range(rad, gE0 - rad))
+        chunks = [s.own_hi - s.own_lo for s in parts]
+        if all(c % h == 0 for c in chunks[:-1]):
+            assert min(chunks) >= G
+    assert all((s.own_hi - s.own_lo) % 64 == 0 for s in slab.partition_aligned(1540, 2, 8, 6, 64)[:-1])
+
+
 def test_partition_rejects_thin_slabs():
     with pytest.raises(ValueError):
         slab.partition(20, 1, 8, 6)

@@ -41,3 +41,11 @@ for what in "$@"; do
       done ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    boxhi)
+      for w in box3d2r-f32-512 box3d3r-f32-512 box3d4r-f32-512 box3d3r-f64-512 box3d4r-f64-512; do
+        python bench.py --workload $w --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_boxhi.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done ;;
+  esac
+done
