@@ -1044,14 +1044,27 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         const int64_t launches0 = p->launches;
         // one warm-up sweep + two timed sweeps of a configuration: seconds per cell-step (1e300 if
         // it cannot run)
+        // one warm-up sweep, then timed sweeps until >= 3 ms (at least 2, at most 16): short sweeps
+        // measured twice were too noisy to order candidates within ~10 % (round-2 suite)
         auto measure = [&](const an5d_config& c0, an5d_config& c) -> double {
             if (resolve_config(*p, dm, T, &c0, c) != AN5D_OK) return 1e300;
-            bool ok = launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
-                                   nullptr, nullptr, st) == AN5D_OK;
+            auto sweep = [&]() {
+                return launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
+                                    nullptr, nullptr, st) == AN5D_OK;
+            };
+            bool ok = sweep();
             cudaEventRecord(e0, st);
-            for (int r = 0; r < 2 && ok; ++r)
-                ok = launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
-                                  nullptr, nullptr, st) == AN5D_OK;
+            ok = ok && sweep();
+            cudaEventRecord(e1, st);
+            if (cudaEventSynchronize(e1) != cudaSuccess || !ok) {
+                cudaGetLastError();
+                return 1e300;
+            }
+            float ms1 = 0;
+            cudaEventElapsedTime(&ms1, e0, e1);
+            const int n = std::max(2, std::min(16, (int)std::ceil(3.0 / std::max(ms1, 1e-3f))));
+            cudaEventRecord(e0, st);
+            for (int r = 0; r < n && ok; ++r) ok = sweep();
             cudaEventRecord(e1, st);
             if (cudaEventSynchronize(e1) != cudaSuccess || !ok) {
                 cudaGetLastError();
@@ -1059,8 +1072,28 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             }
             float ms = 0;
             cudaEventElapsedTime(&ms, e0, e1);
-            return ms * 1e-3 / 2.0 / ((double)interior * c.bT);
+            return ms * 1e-3 / n / ((double)interior * c.bT);
         };
+        // bring the clocks up before the first candidate is timed (~50 ms of the model's pick)
+        {
+            an5d_config c{};
+            if (resolve_config(*p, dm, T, &cand.front(), c) == AN5D_OK) {
+                cudaEventRecord(e0, st);
+                for (int r = 0; r < 64; ++r) {
+                    launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad, nullptr,
+                                 nullptr, st);
+                    if (r == 0) {
+                        cudaEventRecord(e1, st);
+                        cudaEventSynchronize(e1);
+                        float ms = 0;
+                        cudaEventElapsedTime(&ms, e0, e1);
+                        if (ms * 64 > 50.0f) r = 64 - std::max(1, (int)(50.0f / std::max(ms, 1e-3f)));
+                    }
+                }
+                cudaStreamSynchronize(st);
+                cudaGetLastError();
+            }
+        }
         for (const an5d_config& c0 : cand) {
             an5d_config c{};
             const double t = measure(c0, c);

@@ -11,9 +11,14 @@ cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, b
                      cudaStream_t st) {
     Coeffs2D<T, R> cf;
     const T* c = static_cast<const T*>(coeffs);
-    for (int i = 0; i < (2 * R + 1) * (2 * R + 1); ++i) {
+    constexpr int W = 2 * R + 1;
+    for (int i = 0; i < W * W; ++i) {
         if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
         else cf.c[i] = c[i];
+    }
+    for (int dy = 0; dy < W; ++dy) {   // mixed pairs (c[dy][+1], c[dy][-1]) for the swapped FFMA2
+        if constexpr (sizeof(T) == 4) cf.c[W * W + dy] = make_float2(c[dy * W + R + 1], c[dy * W + R - 1]);
+        else cf.c[W * W + dy] = 0;
     }
     constexpr size_t smem = smem_bytes_2d<T, R, BT, V, ASSOC, NW>();
     auto fn = &an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW>;

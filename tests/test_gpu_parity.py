@@ -517,19 +517,7 @@ def _ipc_worker(rank, ws, port, name, n_int, T, bT, dtype_name, out_path):
     b = an5d.empty_grid(loc.shape, rad, dtype)
     flag = torch.zeros(32, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
-    mine = [an5d.ipc_export(t.data_ptr()) for t in (a, b, flag)]
-    allh = [None] * ws
-    dist.all_gather_object(allh, mine)
-    opened, links = [], {}
-    for side, k in (("lo", rank - 1), ("hi", rank + 1)):
-        if 0 <= k < ws:
-            ptrs = []
-            for h, off in allh[k]:
-                base = an5d.ipc_open(h)
-                opened.append(base)
-                ptrs.append(base + off)
-            links[side] = slab.PeerLink((ptrs[0], ptrs[1]), s.loc_lo - parts[k].loc_lo, ptrs[2])
-    fl = slab.FusedLinks(links.get("lo"), links.get("hi"), flag.data_ptr())
+    fl, opened = slab.connect_fused(parts, rank, (a, b), flag)
     dist.barrier()
     out = slab.run_fused(st, s, (a, b), T, cfg, fl, stream=torch.cuda.current_stream())
     torch.cuda.synchronize()

@@ -49,3 +49,15 @@ for what in "$@"; do
       done ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    split1)
+      for n in 32 64; do
+        python bench.py --workload star2d1r-f32-16384 --nthr $n --steps 3 --warmup 2 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_split1.jsonl 2>> gpurun_out/${TAG}_suite.err
+        python bench.py --workload star2d1r-f32-16384 --nthr $n --bt 7 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_split1.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done
+      for w in j3d27pt-f64-512 box3d1r-f64-512 star3d3r-f64-512 box3d4r-f32-512 box3d4r-f64-512 box3d3r-f32-512; do
+        python bench.py --workload $w --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_split1.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done ;;
+  esac
+done
