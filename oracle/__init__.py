@@ -11,7 +11,8 @@ Contents
   * :mod:`oracle.geometry` -- the paper's blocking bookkeeping formulas
     written out independently of the library's C++ (bit-exact checks of an5d_describe /
     an5d_schedule).
-  * :mod:`oracle.model` -- the paper's section-5 performance model in "V100 mode".
+(The paper's section-5 performance model lives in the library, an5d_model_paper, and is pinned
+directly to Table 5's printed "Model" column by tests/test_model_paper.py.)
 
 Pins (tests/test_oracle_pins.py) tie this oracle to values fixed by the paper and mathematics:
 constant field, linear field, quadratic closed form, mirrored impulse, T-fold self-convolution,

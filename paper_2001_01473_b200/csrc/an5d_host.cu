@@ -61,8 +61,6 @@ struct Plan {
     std::vector<double> coeffs_folded; // dense table / divisor (P:596-602 reciprocal folding)
     std::vector<unsigned char> coeffs_dev_t;  // rounded to dtype, as raw bytes
     double divisor;
-    cudaStream_t side = nullptr;       // edge-tile launches run here, concurrently
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int device = -1;
     int64_t launches = 0;
     unsigned long long* ctr = nullptr;  // kCtrRing dynamic-scheduling counter pairs (device, zeroed)
@@ -554,19 +552,12 @@ an5d_status launch_copy(Plan& p, const void* src, void* dst, const Dims& dm, boo
     return e == cudaSuccess ? AN5D_OK : cuda_fail(e, "copy kernel launch");
 }
 
+// Per-device plan state: the dynamic-scheduling counter pairs (zeroed) and the run-table cache.
 an5d_status ensure_streams(Plan& p) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    if (p.side && p.device == dev) return AN5D_OK;
-    if (p.side) {
-        cudaStreamDestroy(p.side);
-        cudaEventDestroy(p.ev_fork);
-        cudaEventDestroy(p.ev_join);
-    }
-    if ((e = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
-    if ((e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
-    if ((e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    if (p.ctr && p.device == dev) return AN5D_OK;
     if (p.ctr) cudaFree(p.ctr);
     for (auto& kv : p.runs) cudaFree(kv.second.first);
     p.runs.clear();
@@ -609,7 +600,7 @@ an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src,
     return AN5D_OK;
 }
 
-// One sweep: edge units on the side stream, interior units on the caller's stream, joined.
+// One sweep: one persistent launch (2D) or one block per run-table unit (3D), on the caller's stream.
 // Peer-store fields of a sweep's argument block (fused halo exchange): element shifts from the
 // per-plane strides.  Planes [out_lo, out_lo + n0) also go to the lower neighbour, [out_hi - n1,
 // out_hi) to the upper one.
@@ -947,11 +938,6 @@ an5d_status an5d_destroy(an5d_plan* p) {
     if (!p) return AN5D_OK;
     if (p->ctr) cudaFree(p->ctr);
     for (auto& kv : p->runs) cudaFree(kv.second.first);
-    if (p->side) {
-        cudaStreamDestroy(p->side);
-        cudaEventDestroy(p->ev_fork);
-        cudaEventDestroy(p->ev_join);
-    }
     delete p;
     return AN5D_OK;
 }

@@ -61,6 +61,40 @@ def test_valid_region_recurrence():
                 assert og.valid_region(bS, T + 1, rad) == og.valid_region(bS, T, rad) - 2 * rad
 
 
+def test_valid_region_brute_force_dependency_cone():
+    """P:336 'the size of the region with valid computation ... b_S - 2 T rad': brute force on
+    position SETS (no formula) -- a cell is valid at level T when all its stencil inputs were valid
+    at level T-1, starting from the whole loaded tile at T = 0 -- gives exactly the cells
+    [T rad, b_S - T rad), and the compute region is the level-b_T set."""
+    for bS in (7, 16, 33, 64):
+        for rad in (1, 2, 3, 4):
+            valid = set(range(bS))
+            for T in range(1, 9):
+                valid = {x for x in valid if all(x + d in valid for d in range(-rad, rad + 1))}
+                w = og.valid_region(bS, T, rad)
+                assert len(valid) == max(0, w), (bS, rad, T)
+                if w > 0:
+                    assert valid == set(range(T * rad, bS - T * rad))
+                    assert og.compute_region(bS, T, rad) == len(valid)
+
+
+def test_paper_adjustment_condition_literal_values():
+    """The printed final-block condition '(I_T mod b_T) != 0 or ((I_T / b_T) mod 2) !=
+    (b_T mod 2)', evaluated by hand for a few cases (integer division I_T / b_T):
+      (1000, 4): 0, 250 mod 2 = 0 == 4 mod 2 = 0            -> False
+      (1000, 3): 1000 mod 3 = 1                             -> True
+      (12, 3):   0, 4 mod 2 = 0 != 3 mod 2 = 1              -> True  (fires with an even sweep
+                 count and odd b_T, where reading R-7 needs no fix: SURVEY C-7)
+      (9, 3):    0, 3 mod 2 = 1 == 1                        -> False
+      (10, 10):  0, 1 mod 2 = 1 != 10 mod 2 = 0             -> True
+      (16, 8):   0, 2 mod 2 = 0 == 0                        -> False
+      (7, 2):    7 mod 2 = 1                                -> True"""
+    cases = {(1000, 4): False, (1000, 3): True, (12, 3): True, (9, 3): False, (10, 10): True, (16, 8): False,
+             (7, 2): True}
+    for (IT, bT), want in cases.items():
+        assert og.paper_adjustment_condition(IT, bT) is want, (IT, bT)
+
+
 @pytest.mark.parametrize("case", _gold("schedule_survey.json")["cases"])
 def test_schedule_matches_survey_table(case, an5d):
     """Library (C++) and oracle (Python) schedules equal SURVEY's independently computed table."""

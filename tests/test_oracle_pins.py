@@ -198,3 +198,27 @@ def test_threads_do_not_change_result():
     a = oracle.run(g, 1, inputs.BOX, tab, div, 11, np.float32, nthreads=1)
     b = oracle.run(g, 1, inputs.BOX, tab, div, 11, np.float32, nthreads=3)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("ndim,rad,shape", [(2, 1, inputs.STAR), (2, 3, inputs.BOX), (3, 1, inputs.BOX),
+                                            (3, 2, inputs.STAR)])
+def test_steps_match_scipy_correlate_exact_integers(ndim, rad, shape):
+    """An independent library routine as the reference: each time step is
+    scipy.ndimage.correlate (out[x] = sum_d w[d] in[x + d], the definition of fig:jacobi2d /
+    Table 2 with the ring held fixed), applied to the interior.  Integer taps and {-1, 0, 1}
+    inputs keep every value an exact integer in fp64, so any summation order gives the same bits
+    and the oracle must equal it exactly over several steps."""
+    from scipy import ndimage
+    tab, div = inputs.coeff_table(ndim, rad, shape, seed=12, kind="pm1")
+    ext = tuple(9 + 2 * rad for _ in range(ndim))
+    g = inputs.global_grid(3, ext, kind="pm")
+    T = 3
+    cur = g.copy()
+    core = tuple(slice(rad, e - rad) for e in ext)
+    for _ in range(T):
+        nxt = cur.copy()
+        nxt[core] = ndimage.correlate(cur, tab, mode="constant", cval=0.0)[core] / div
+        cur = nxt
+    got = oracle.run(g, rad, shape, tab, div, T, np.float64)
+    assert np.abs(cur).max() < 2 ** 50
+    assert np.array_equal(got, cur)

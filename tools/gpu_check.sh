@@ -61,3 +61,15 @@ for what in "$@"; do
       done ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    ab2d)
+      for rep in 1 2; do
+        python bench.py --workload star2d1r-f32-16384 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_ab2d.jsonl 2>> gpurun_out/${TAG}_suite.err
+        AN5D_LIB=$PWD/paper_2001_01473_b200/libAN5D_noswap.so python bench.py --workload star2d1r-f32-16384 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_ab2d_noswap.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done
+      for w in box3d1r-f64-512 j3d27pt-f64-512 star3d1r-f64-512 star2d2r-f32-16384 box2d1r-f32-16384; do
+        python bench.py --workload $w --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_ab2d.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done ;;
+  esac
+done
