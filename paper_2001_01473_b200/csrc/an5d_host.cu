@@ -994,26 +994,29 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         if (h.bT < 0 || h.vec < 0 || h.h < 0 || (h.direct != 0 && h.direct != 1))
             return fail(AN5D_ERR_INVALID_ARGUMENT, "bad hint");
         const auto ranked = rank_configs(*p, dm, T, &h);
+        // candidates: the top_k distinct (b_T, vec) pairs of the model's ranking, each with the
+        // model's best configuration of EVERY kernel layout (threads x tile width) it has, plus
+        // the best configuration of any layout still missing.  The model orders b_T well but the
+        // layouts only roughly (measured on B200: the 2D level split ranks high in the model and
+        // runs 8-20 % slower; the 512-thread fp64 3D layout runs 15-30 % faster), so every layout
+        // is measured rather than ranked.
+        auto layout_of = [&](const an5d_config& c) { return std::make_tuple(c.vec, c.n_thr, cfg_tile_x(*p, c)); };
+        std::vector<std::pair<int, int>> pairs;
+        for (const auto& r : ranked) {
+            const std::pair<int, int> bv(r.second.bT, r.second.vec);
+            if (std::find(pairs.begin(), pairs.end(), bv) == pairs.end()) pairs.push_back(bv);
+            if ((int)pairs.size() >= top_k) break;
+        }
         std::vector<an5d_config> cand;
-        for (const auto& r : ranked) {
-            bool seen = false;
-            for (const auto& c : cand)
-                seen = seen || (c.bT == r.second.bT && c.vec == r.second.vec && c.n_thr == r.second.n_thr &&
-                                c.bS[0] == r.second.bS[0] && c.bS[1] == r.second.bS[1]);
-            if (!seen) cand.push_back(r.second);
-            if ((int)cand.size() >= top_k) break;
-        }
-        // ... plus the model's best configuration of every kernel layout (vec, threads, tile
-        // width) the top k missed: the model ranks layouts only roughly (measured on B200: the
-        // 512-thread fp64 3D layout is 15-30 % faster, but its model rank varies by stencil)
-        auto layout_of = [&](const an5d_config& c) {
-            return std::make_tuple(c.vec, c.n_thr, cfg_tile_x(*p, c));
+        auto add_if_new_layout = [&](const an5d_config& c, bool same_bT) {
+            for (const auto& x : cand)
+                if (layout_of(x) == layout_of(c) && (!same_bT || x.bT == c.bT)) return;
+            cand.push_back(c);
         };
-        for (const auto& r : ranked) {
-            bool have = false;
-            for (const auto& c : cand) have = have || layout_of(c) == layout_of(r.second);
-            if (!have) cand.push_back(r.second);
-        }
+        for (const auto& r : ranked)
+            if (std::find(pairs.begin(), pairs.end(), std::make_pair(r.second.bT, r.second.vec)) != pairs.end())
+                add_if_new_layout(r.second, true);
+        for (const auto& r : ranked) add_if_new_layout(r.second, false);
         if (cand.empty())
             return fail(AN5D_ERR_UNSUPPORTED, "no feasible kernel instance for ndim=%d rad=%d shape=%d dtype=%d",
                         p->ndim, p->rad, p->shape, p->dtype);
@@ -1030,8 +1033,10 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         const int64_t launches0 = p->launches;
         // one warm-up sweep + two timed sweeps of a configuration: seconds per cell-step (1e300 if
         // it cannot run)
-        // one warm-up sweep, then timed sweeps until >= 3 ms (at least 2, at most 16): short sweeps
-        // measured twice were too noisy to order candidates within ~10 % (round-2 suite)
+        // one warm-up sweep, then timed sweeps for >= 8 ms (at least 2, at most 64); every candidate
+        // is timed twice, in opposite orders, and scored by its faster pass: under the 1 kW power
+        // cap the clocks drift by up to 10 % within a tune, which ordered short single passes by
+        // the candidates' position rather than their speed (round-2 measurements)
         auto measure = [&](const an5d_config& c0, an5d_config& c) -> double {
             if (resolve_config(*p, dm, T, &c0, c) != AN5D_OK) return 1e300;
             auto sweep = [&]() {
@@ -1048,7 +1053,7 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             }
             float ms1 = 0;
             cudaEventElapsedTime(&ms1, e0, e1);
-            const int n = std::max(2, std::min(16, (int)std::ceil(3.0 / std::max(ms1, 1e-3f))));
+            const int n = std::max(2, std::min(64, (int)std::ceil(8.0 / std::max(ms1, 1e-3f))));
             cudaEventRecord(e0, st);
             for (int r = 0; r < n && ok; ++r) ok = sweep();
             cudaEventRecord(e1, st);
@@ -1080,23 +1085,39 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
                 cudaGetLastError();
             }
         }
-        for (const an5d_config& c0 : cand) {
-            an5d_config c{};
-            const double t = measure(c0, c);
-            if (t < best) {
-                best = t;
-                bc = c;
+        const bool tlog = getenv("AN5D_TUNE_LOG") != nullptr;   // debug: every candidate's time
+        std::vector<double> score(cand.size(), 1e300);
+        std::vector<an5d_config> resolved(cand.size());
+        for (int pass = 0; pass < 2; ++pass)
+            for (size_t j = 0; j < cand.size(); ++j) {
+                const size_t q = pass == 0 ? j : cand.size() - 1 - j;
+                const double t = measure(cand[q], resolved[q]);
+                score[q] = std::min(score[q], t);
+                if (tlog)
+                    fprintf(stderr, "an5d_tune: pass %d bT %d vec %d n_thr %d bS %d,%d h %lld -> %.4g ps/cell-step\n",
+                            pass, cand[q].bT, cand[q].vec, cand[q].n_thr, cand[q].bS[0], cand[q].bS[1],
+                            (long long)cand[q].h, t * 1e12);
             }
-        }
+        for (size_t q = 0; q < cand.size(); ++q)
+            if (score[q] < best) {
+                best = score[q];
+                bc = resolved[q];
+            }
         // stream-block length refinement around the model's pick for the winning (b_T, V) (the
         // model ranks h coarsely; measured on B200, star2d1r b_T 7: h 48 beats the model's 60 by 1.5 %)
         if (!h.h && best < 1e299) {
             const an5d_config base = bc;
+            {   // re-time the winner so its neighbours are compared under the same clocks
+                an5d_config c{};
+                const double t = measure(base, c);
+                if (t < 1e299) best = t;
+            }
             for (double f : {0.5, 0.75, 1.5}) {
                 an5d_config c0 = base, c{};
                 c0.h = std::max<int64_t>(8, (int64_t)std::llround((double)base.h * f));
                 if (c0.h == base.h) continue;
                 const double t = measure(c0, c);
+                if (tlog) fprintf(stderr, "an5d_tune: refine h %lld -> %.4g ps/cell-step\n", (long long)c0.h, t * 1e12);
                 if (t < best) {
                     best = t;
                     bc = c;
