@@ -399,7 +399,14 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     const int64_t rows_per_unit = g.h + 2LL * bT * R;
     int64_t cells_per_plane = 1;
     for (int i = 0; i < p.ndim - 1; ++i) cells_per_plane *= g.loaded[i];
-    const double eta_hbm = 0.75, eta_fma = p.ndim == 2 ? 0.45 : 0.35;
+    // steady-state fractions of the measured peaks the kernels reach on B200, per layout
+    // (round 1-2 suites): 2D one warp per tile 0.45 of the FMA peak, the two-warp level split
+    // 0.88x that; 3D 256-thread blocks 0.35, 512-thread fp64 blocks (twice the warps) 1.25x,
+    // 512-thread fp32 128-wide tiles 0.87x
+    const double eta_hbm = 0.75;
+    double eta_fma = p.ndim == 2 ? 0.45 : 0.35;
+    if (p.ndim == 2 && inst.threads == 64) eta_fma *= 0.88;
+    if (p.ndim == 3 && inst.threads == 512) eta_fma *= p.dtype == AN5D_F64 ? 1.25 : 0.87;
     const double resident = (double)resident_blocks(inst) * di.n_sm;
     // units are runs of stream blocks (build_runs_2d / _3d); each run pays the overlap once
     double units = (double)g.n_units, unit_rows = (double)rows_per_unit;

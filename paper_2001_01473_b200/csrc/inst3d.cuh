@@ -17,6 +17,11 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
         if constexpr (sizeof(T) == 4) cf.c[i] = make_float2(c[i], c[i]);   // broadcast pair (FFMA2)
         else cf.c[i] = c[i];
     }
+    constexpr int W = 2 * R + 1;
+    for (int r = 0; r < W * W; ++r) {   // mixed pairs (c[dz][dy][+1], c[dz][dy][-1]), r = (dz+R) W + (dy+R)
+        if constexpr (sizeof(T) == 4) cf.c[N + r] = make_float2(c[r * W + R + 1], c[r * W + R - 1]);
+        else cf.c[N + r] = 0;
+    }
     auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (!attr_set) {

@@ -133,7 +133,10 @@ struct Unit3D {
 };
 
 template <typename T, int R>
-using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * (2 * R + 1)>;
+using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * (2 * R + 1) + (2 * R + 1) * (2 * R + 1)>;
+// Entries [0, W^3): the dense table (fp32: broadcast pairs); W^3 + (dz+R) W + (dy+R), fp32 only:
+// the mixed pair (c[dz][dy][+1], c[dz][dy][-1]) for the swapped-operand FFMA2 of the dx = +-1
+// taps (see kernel2d.cuh Coeffs2D).
 
 template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_>
 __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
@@ -419,10 +422,31 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                                 }
                             }
                         };
+                        const E* cmix = &cf.c[W * W * W + (2 * R - j) * W];
 #pragma unroll
                         for (int dy = -R; dy <= R; ++dy)
 #pragma unroll
-                            for (int dx = -R; dx <= R; ++dx) tap_to(acc[L - 1][0], cz[(dy + R) * W + (dx + R)], dy, dx);
+                            for (int dx = -R; dx <= R; ++dx) {
+                                if constexpr (sizeof(T) == 4) {
+                                    if (dx == 1) continue;
+                                    if (dx == -1) {   // dx = -1 and +1 together (swapped-operand FFMA2)
+                                        const E cm = cz[(dy + R) * W + R - 1], cp = cz[(dy + R) * W + R + 1];
+                                        const E mix = cmix[dy + R];
+#pragma unroll
+                                        for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                                            for (int e = 0; e < NE; ++e) {
+                                                E& o = acc[L - 1][0][yy][e];
+                                                const E q = rowref(yy + dy)[e];
+                                                o.x = fmaf(cm.x, X(yy + dy, 2 * e - 1), o.x);
+                                                o.y = fmaf(cp.x, X(yy + dy, 2 * e + 2), o.y);
+                                                o = LN::fma(mix, make_float2(q.y, q.x), o);
+                                            }
+                                        continue;
+                                    }
+                                }
+                                tap_to(acc[L - 1][0], cz[(dy + R) * W + (dx + R)], dy, dx);
+                            }
                         // rotate the slots left by one: the next plane's target moves to slot 0
                         E t0[VY][NE];
 #pragma unroll
@@ -476,11 +500,33 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                         }
                     };
                     auto C = [&](int dy, int dx) { return cf.c[((dz + R) * W + (dy + R)) * W + (dx + R)]; };
+                    // dx = -1 and +1 of one row together (fp32): outer products scalar, inner ones
+                    // one FFMA2 on the pair with swapped halves (kernel2d.cuh Coeffs2D)
+                    [[maybe_unused]] auto tap_pm1 = [&](int dy, bool first) {
+                        if constexpr (sizeof(T) == 4) {
+                            const E cm = C(dy, -1), cp = C(dy, 1), mix = cf.c[W * W * W + (dz + R) * W + (dy + R)];
+#pragma unroll
+                            for (int yy = 0; yy < VY; ++yy)
+#pragma unroll
+                                for (int e = 0; e < NE; ++e) {
+                                    E& o = acc[L - 1][slot][yy][e];
+                                    const E q = rowref(yy + dy)[e];
+                                    o.x = first ? cm.x * X(yy + dy, 2 * e - 1) : fmaf(cm.x, X(yy + dy, 2 * e - 1), o.x);
+                                    o.y = first ? cp.x * X(yy + dy, 2 * e + 2) : fmaf(cp.x, X(yy + dy, 2 * e + 2), o.y);
+                                    o = LN::fma(mix, make_float2(q.y, q.x), o);
+                                }
+                        }
+                    };
+                    constexpr bool PM1 = sizeof(T) == 4;
                     if constexpr (BOX) {
 #pragma unroll
                         for (int dy = -R; dy <= R; ++dy)
 #pragma unroll
-                            for (int dx = -R; dx <= R; ++dx) tap(C(dy, dx), dy, dx, dz == -R && dy == -R && dx == -R);
+                            for (int dx = -R; dx <= R; ++dx) {
+                                if (PM1 && dx == 1) continue;
+                                if (PM1 && dx == -1) tap_pm1(dy, dz == -R && dy == -R && R == 1);
+                                else tap(C(dy, dx), dy, dx, dz == -R && dy == -R && dx == -R);
+                            }
                     } else if constexpr (dz != 0) {
                         tap(C(0, 0), 0, 0, dz == -R);
                     } else {
@@ -488,7 +534,11 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
                         for (int dy = -R; dy < 0; ++dy) tap(C(dy, 0), dy, 0, false);
 #pragma unroll
-                        for (int dx = -R; dx <= R; ++dx) tap(C(0, dx), 0, dx, false);
+                        for (int dx = -R; dx <= R; ++dx) {
+                            if (PM1 && dx == 1) continue;
+                            if (PM1 && dx == -1) tap_pm1(0, false);
+                            else tap(C(0, dx), 0, dx, false);
+                        }
 #pragma unroll
                         for (int dy = 1; dy <= R; ++dy) tap(C(dy, 0), dy, 0, false);
                     }
