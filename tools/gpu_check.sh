@@ -73,3 +73,19 @@ for what in "$@"; do
       done ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    suiteall)
+      python bench.py --suite all,config4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_suite.jsonl 2>> gpurun_out/${TAG}_suite.err ;;
+    swapab)
+      for rep in 1 2 3; do
+        python bench.py --bt 7 --h 45 --nthr 32 --no-tune --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_swapab.jsonl 2>> gpurun_out/${TAG}_suite.err
+        AN5D_LIB=$PWD/paper_2001_01473_b200/libAN5D_noswap.so python bench.py --bt 7 --h 45 --nthr 32 --no-tune --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_swapab_noswap.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done ;;
+    ncufinal)
+      ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
+          python bench.py --bt 7 --h 45 --nthr 32 --no-tune --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_bench.log 2>&1
+      ncu --set full --clock-control none --import-source on -k regex:an5d_sweep -s 4 -c 1 -o gpurun_out/${TAG}_prof_headline \
+          python tools/sweeponly.py star2d1r f32 7 45 8 6 32 > gpurun_out/${TAG}_ncu_full.log 2>&1 ;;
+  esac
+done
