@@ -191,6 +191,28 @@ an5d_status an5d_ipc_export(const void* ptr, void* handle64, int64_t* offset);
 an5d_status an5d_ipc_open(const void* handle64, void** base);
 an5d_status an5d_ipc_close(void* base);
 
+/* The whole T-step run of one slab with the fused exchange, stream-ordered on cuda_stream (the
+ * library-owned multi-GPU data plane; no NCCL):  ring copy of the GLOBAL ring planes/cells, then
+ * per sweep i: wait until each neighbour's flag >= epoch + i, an5d_sweep_peer over the owned planes
+ * [own_lo, own_hi) (local indices) storing d_next*rad boundary planes into the neighbours'
+ * buffers of dst's parity, write own flag = epoch + i + 1.  On return links->epoch has advanced by
+ * the number of sweeps (every rank must run the same T and b_T); grid_out's owned planes hold step
+ * T once the stream reaches that point.  CUDA-graph capturable (flags, kernels and copies only).
+ * Errors as an5d_sweep_peer; AN5D_ERR_INVALID_ARGUMENT if a side gives buffers without a flag.   */
+typedef struct {
+    void* peer_bufs[2][2];        /* [0 lower / 1 upper][the neighbour's buffer paired with grid_in, */
+                                  /* with grid_out]: device pointers valid here, or NULL            */
+    int64_t peer_plane_shift[2];  /* my outer_offset - the neighbour's outer_offset                */
+    uint32_t* peer_flag[2];       /* the neighbours' progress flags (peer-mapped), or NULL          */
+    uint32_t* flag;               /* this slab's progress flag (device memory)                      */
+    uint32_t epoch;               /* sweeps every slab completed before this run (in / out)         */
+} an5d_slab_links;
+
+an5d_status an5d_run_slab(an5d_plan* plan, void* grid_in, void* grid_out, const int64_t* extents,
+                          const int64_t* pitches, int64_t T, const an5d_config* cfg, int64_t outer_offset,
+                          int64_t global_outer_extent, int64_t own_lo, int64_t own_hi,
+                          an5d_slab_links* links, void* cuda_stream);
+
 /* Copy the rad-wide ring cells of src into dst (O(surface) kernel).  With outer_offset /
  * global_outer_extent as in an5d_sweep, only global ring planes/rows/columns are copied.       */
 an5d_status an5d_copy_ring(an5d_plan* plan, const void* src, void* dst, const int64_t* extents,

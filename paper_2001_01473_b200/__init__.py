@@ -66,6 +66,11 @@ class PeerStore(ctypes.Structure):
                 ("send_planes", ctypes.c_int64 * 2)]
 
 
+class SlabLinks(ctypes.Structure):
+    _fields_ = [("peer_bufs", (ctypes.c_void_p * 2) * 2), ("peer_plane_shift", ctypes.c_int64 * 2),
+                ("peer_flag", ctypes.c_void_p * 2), ("flag", ctypes.c_void_p), ("epoch", ctypes.c_uint32)]
+
+
 class DeviceParams(ctypes.Structure):
     _fields_ = [("n_sm", ctypes.c_int), ("max_threads_per_sm", ctypes.c_int), ("peak_comp_gflops", ctypes.c_double),
                 ("peak_gm_gbs", ctypes.c_double), ("peak_sm_gbs", ctypes.c_double)]
@@ -99,6 +104,8 @@ def _load():
         "an5d_copy_ring": (I32, [P, P, P, pi64, pi64, I64, I64, P]),
         "an5d_sweep_peer": (I32, [P, P, P, pi64, pi64, I32, ctypes.POINTER(Config), I64, I64, I64, I64,
                                   ctypes.POINTER(PeerStore), P, P]),
+        "an5d_run_slab": (I32, [P, P, P, pi64, pi64, I64, ctypes.POINTER(Config), I64, I64, I64, I64,
+                                ctypes.POINTER(SlabLinks), P]),
         "an5d_stream_signal": (I32, [P, ctypes.c_uint32, P]),
         "an5d_stream_wait": (I32, [P, ctypes.c_uint32, P]),
         "an5d_ipc_export": (I32, [P, P, pi64]),
@@ -149,7 +156,7 @@ def load():
 def loaded() -> bool:
     return _LazyLib._h is not None
 
-EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_stream_signal",
+EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_run_slab", "an5d_stream_signal",
                     "an5d_stream_wait", "an5d_ipc_export", "an5d_ipc_open", "an5d_ipc_close", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
                     "an5d_describe", "an5d_schedule", "an5d_model_paper", "an5d_model_paper_search",
                     "an5d_last_launch_count", "an5d_destroy", "an5d_last_error", "an5d_version")
@@ -335,6 +342,30 @@ class Stencil:
         _check(_lib.an5d_sweep(self._h, src.data_ptr(), dst.data_ptr(), _i64(ext), _i64(pit), int(degree),
                                ctypes.byref(c), int(outer_offset), int(g), int(lo), int(hi), wc,
                                ctypes.c_void_p(st.cuda_stream)))
+
+    def run_slab(self, grid_in: torch.Tensor, grid_out: torch.Tensor, T: int, cfg, outer_offset: int,
+                 global_outer_extent: int, own_lo: int, own_hi: int, lo=None, hi=None, flag: int = 0, epoch: int = 0,
+                 stream=None) -> int:
+        """One slab's T-step run with the fused halo exchange (an5d_run_slab).  ``lo`` / ``hi``:
+        None or (neighbour buffer paired with grid_in, with grid_out, plane shift, flag pointer).
+        Returns the new epoch."""
+        ext, pit = _geom_of(grid_in)
+        st = stream if stream is not None else torch.cuda.current_stream(grid_in.device)
+        L = SlabLinks()
+        for k, side in enumerate((lo, hi)):
+            if side:
+                b_in, b_out, shift, fl = side
+                L.peer_bufs[k][0] = int(b_in)
+                L.peer_bufs[k][1] = int(b_out)
+                L.peer_plane_shift[k] = int(shift)
+                L.peer_flag[k] = int(fl)
+        L.flag = int(flag)
+        L.epoch = int(epoch)
+        c = _cfg(cfg)
+        _check(_lib.an5d_run_slab(self._h, grid_in.data_ptr(), grid_out.data_ptr(), _i64(ext), _i64(pit), int(T),
+                                  ctypes.byref(c), int(outer_offset), int(global_outer_extent), int(own_lo),
+                                  int(own_hi), ctypes.byref(L), ctypes.c_void_p(st.cuda_stream)))
+        return int(L.epoch)
 
     def copy_ring(self, src: torch.Tensor, dst: torch.Tensor, outer_offset: int = 0,
                   global_outer_extent: int | None = None, stream=None):

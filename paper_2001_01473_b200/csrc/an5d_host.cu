@@ -629,9 +629,11 @@ void set_peers(Args& a, const an5d_peer_store* ps, int64_t plane_stride, int64_t
     }
 }
 
+// dry = true: everything up to the launch (geometry, run-table upload), no launch -- lets a caller
+// upload the run tables of all its sweeps before it enqueues stream waits (an5d_run_slab).
 an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, int d, const an5d_config& cfg,
                          int64_t g_off, int64_t gE0, int64_t out_lo, int64_t out_hi, int32_t* wc,
-                         const an5d_peer_store* peers,
+                         const an5d_peer_store* peers, bool dry,
                          cudaStream_t st) {
     const Instance* inst = find_instance(p, d, cfg);
     if (!inst) return fail(AN5D_ERR_UNSUPPORTED, "no kernel instance for degree %d vec %d", d, cfg.vec);
@@ -674,6 +676,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
             a.runs = it->second.first;
             a.n_units = it->second.second;
         }
+        if (dry) return AN5D_OK;
         // AN5D_UNIT_PROFILE=path: debug-only per-unit timing dump (synchronises; never in benches)
         const char* prof_path = getenv("AN5D_UNIT_PROFILE");
         if (prof_path && !wc) cudaMalloc(&a.unit_ns, sizeof(long long) * 3 * a.n_units);
@@ -726,6 +729,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
             a.runs = it->second.first;
             a.n_units = it->second.second;
         }
+        if (dry) return AN5D_OK;
         a.Ey = (int)dm.E[1]; a.Ex = (int)dm.E[2];
         a.Cy = g.C[0]; a.Cx = g.C[1]; a.Hy = g.halo[0]; a.Hx = g.halo[1];
         a.nty = (int)g.ntiles[0]; a.ntx = (int)g.ntiles[1];
@@ -1048,7 +1052,7 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             if (resolve_config(*p, dm, T, &c0, c) != AN5D_OK) return 1e300;
             auto sweep = [&]() {
                 return launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad,
-                                    nullptr, nullptr, st) == AN5D_OK;
+                                    nullptr, nullptr, false, st) == AN5D_OK;
             };
             bool ok = sweep();
             cudaEventRecord(e0, st);
@@ -1079,7 +1083,7 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
                 cudaEventRecord(e0, st);
                 for (int r = 0; r < 64; ++r) {
                     launch_sweep(*p, grid_in, grid_out, dm, c.bT, c, 0, dm.E[0], p->rad, dm.E[0] - p->rad, nullptr,
-                                 nullptr, st);
+                                 nullptr, false, st);
                     if (r == 0) {
                         cudaEventRecord(e1, st);
                         cudaEventSynchronize(e1);
@@ -1245,7 +1249,7 @@ an5d_status an5d_sweep_peer(an5d_plan* p, const void* src, void* dst, const int6
         if ((s = resolve_config(*p, dm, 0, cfg, c)) != AN5D_OK) return s;
         if ((s = ensure_streams(*p)) != AN5D_OK) return s;
         return launch_sweep(*p, src, dst, dm, degree, c, outer_offset, global_outer_extent, out_lo, out_hi,
-                            debug_write_count, peers, (cudaStream_t)stream);
+                            debug_write_count, peers, false, (cudaStream_t)stream);
     } catch (...) {
         return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
     }
@@ -1338,12 +1342,85 @@ an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t*
             const void* src = bufs[i % 2];
             void* dst = bufs[(i + 1) % 2];
             if ((s = launch_sweep(*p, src, dst, dm, deg[i], c, 0, dm.E[0], p->rad, dm.E[0] - p->rad, nullptr, nullptr,
-                                  st)) !=
+                                  false, st)) !=
                 AN5D_OK)
                 return s;
         }
         if (tc) {
             if ((s = launch_copy(*p, grid_in, grid_out, dm, false, 0, dm.E[0], st)) != AN5D_OK) return s;
+        }
+        return AN5D_OK;
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_run_slab(an5d_plan* p, void* grid_in, void* grid_out, const int64_t* extents, const int64_t* pitches,
+                          int64_t T, const an5d_config* cfg, int64_t outer_offset, int64_t global_outer_extent,
+                          int64_t own_lo, int64_t own_hi, an5d_slab_links* links, void* stream) {
+    try {
+        if (!p || !links || !links->flag) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (T < 0) return fail(AN5D_ERR_INVALID_ARGUMENT, "T < 0");
+        Dims dm{};
+        an5d_status s = read_dims(*p, extents, pitches, dm);
+        if (s != AN5D_OK) return s;
+        if ((s = check_alignment(*p, grid_in, dm, "grid_in")) != AN5D_OK) return s;
+        if ((s = check_alignment(*p, grid_out, dm, "grid_out")) != AN5D_OK) return s;
+        if (grid_in == grid_out) return fail(AN5D_ERR_INVALID_ARGUMENT, "grid_in and grid_out must differ");
+        if (own_lo < 0 || own_hi > dm.E[0] || own_hi <= own_lo) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad owned planes");
+        for (int k = 0; k < 2; ++k)
+            if (!links->peer_flag[k] != !links->peer_bufs[k][0] || !links->peer_bufs[k][0] != !links->peer_bufs[k][1])
+                return fail(AN5D_ERR_INVALID_ARGUMENT, "side %d: buffers and flag must be given together", k);
+        cudaStream_t st = (cudaStream_t)stream;
+        an5d_config c{};
+        if ((s = resolve_config(*p, dm, T, cfg, c)) != AN5D_OK) return s;
+        std::vector<int> deg;
+        bool tc = false;
+        make_schedule(T, c.bT, deg, tc);
+        for (int k = 0; k < 2; ++k)   // a neighbour needs b_T rad ghost planes from each side
+            if (links->peer_flag[k] && (own_hi - own_lo) < (int64_t)c.bT * p->rad)
+                return fail(AN5D_ERR_INVALID_ARGUMENT, "slab owns fewer planes than the ghost depth");
+        if ((s = ensure_streams(*p)) != AN5D_OK) return s;
+        // upload every sweep's run table now: a synchronous upload behind a stream wait on a
+        // neighbour that has not been enqueued yet (one process, several slabs) could deadlock
+        {
+            const int64_t lo = std::max(own_lo, (int64_t)p->rad - outer_offset);
+            const int64_t hi = std::min(own_hi, global_outer_extent - p->rad - outer_offset);
+            for (size_t i = 0; i < deg.size() && hi > lo; ++i)
+                if ((s = launch_sweep(*p, grid_in, grid_out, dm, deg[i], c, outer_offset, global_outer_extent, lo, hi,
+                                      nullptr, nullptr, true, st)) != AN5D_OK)
+                    return s;
+        }
+        p->launches = 0;
+        if ((s = launch_copy(*p, grid_in, grid_out, dm, true, outer_offset, global_outer_extent, st)) != AN5D_OK) return s;
+        void* bufs[2] = {grid_in, grid_out};
+        for (size_t i = 0; i < deg.size(); ++i) {
+            const void* src = bufs[i % 2];
+            void* dst = bufs[(i + 1) % 2];
+            const int par = (int)((i + 1) % 2);           // dst is grid_out (1) or grid_in (0)
+            const int nd = i + 1 < deg.size() ? deg[i + 1] : 0;
+            for (int k = 0; k < 2; ++k)
+                if (links->peer_flag[k] &&
+                    (s = an5d_stream_wait(links->peer_flag[k], links->epoch + (uint32_t)i, stream)) != AN5D_OK)
+                    return s;
+            an5d_peer_store ps{};
+            for (int k = 0; k < 2; ++k)
+                if (links->peer_flag[k] && nd) {
+                    ps.peer_dst[k] = links->peer_bufs[k][par];
+                    ps.peer_plane_shift[k] = links->peer_plane_shift[k];
+                    ps.send_planes[k] = (int64_t)nd * p->rad;
+                }
+            if ((s = an5d_sweep_peer(p, src, dst, extents, pitches, deg[i], &c, outer_offset, global_outer_extent,
+                                     own_lo, own_hi, &ps, nullptr, stream)) != AN5D_OK)
+                return s;
+            if ((s = an5d_stream_signal(links->flag, links->epoch + (uint32_t)i + 1, stream)) != AN5D_OK) return s;
+        }
+        links->epoch += (uint32_t)deg.size();
+        if (tc) {   // b_T == 1 with an even sweep count: the owned planes' result is in grid_in
+            const size_t off = (size_t)own_lo * dm.pitch[0] * p->elem, n = (size_t)(own_hi - own_lo) * dm.pitch[0] * p->elem;
+            const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(grid_out) + off, static_cast<char*>(grid_in) + off, n,
+                                                  cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "trailing copy");
         }
         return AN5D_OK;
     } catch (...) {

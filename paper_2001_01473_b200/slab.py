@@ -278,48 +278,17 @@ class FusedLinks:
 
 
 def run_fused(stencil, s: Slab, bufs, T: int, cfg: dict, links: FusedLinks, stream=None, schedule_fn=None):
-    """One rank's share of a T-step run with the fused halo exchange.  Before sweep i a rank waits
-    until both neighbours finished sweep i-1 (flag >= epoch + i): its ghost planes for sweep i are
-    then stored, and the neighbours no longer read the buffer sweep i writes ghosts into.  Sweep i
-    stores the d_next * rad outermost owned planes into the neighbours' buffers of the same parity
-    as its destination; then the rank signals flag = epoch + i + 1.  Returns grid_out (bufs[1])."""
-    import paper_2001_01473_b200 as an5d
-    from . import schedule as lib_schedule
-    degrees, trailing = (schedule_fn or lib_schedule)(T, cfg["bT"])
+    """One rank's share of a T-step run with the fused halo exchange, entirely in the library
+    (an5d_run_slab, stream-ordered): before sweep i a rank waits until both neighbours finished
+    sweep i-1 (flag >= epoch + i) -- its ghost planes for sweep i are then stored, and the
+    neighbours no longer read the buffer sweep i writes ghosts into; sweep i stores the
+    d_next * rad outermost owned planes into the neighbours' buffers of its destination's parity
+    (from the sweep kernel); then the rank writes flag = epoch + i + 1.  Returns grid_out."""
     a, b = bufs
-    st = stream
-    stencil.copy_ring(a, b, outer_offset=s.loc_lo, global_outer_extent=s.gE0, stream=st)
-    for i, d in enumerate(degrees):
-        src, dst = (a, b) if i % 2 == 0 else (b, a)
-        par = (i + 1) % 2                      # parity of dst: 1 = b, 0 = a
-        nd = degrees[i + 1] if i + 1 < len(degrees) else 0
-        g = nd * s.rad
-        for ln in (links.lo, links.hi):
-            if ln is not None:
-                an5d.stream_wait(ln.flag, links.epoch + i, st)
-        peers = {}
-        if links.lo is not None and g:
-            peers["lo"] = (links.lo.bufs[par], links.lo.shift, g)
-        if links.hi is not None and g:
-            peers["hi"] = (links.hi.bufs[par], links.hi.shift, g)
-        stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=s.gE0, out_lo=s.out_lo,
-                      out_hi=s.out_hi, stream=st, peers=peers or None)
-        an5d.stream_signal(links.flag, links.epoch + i + 1, st)
-    links.epoch += len(degrees)
-    if trailing:
-        n = s.out_hi - s.out_lo
-        import torch
-        with torch.cuda.stream(st) if st is not None else _nullctx():
-            _plane_view(b, s.out_lo, n).copy_(_plane_view(a, s.out_lo, n))
+    side = lambda ln: None if ln is None else (ln.bufs[0], ln.bufs[1], ln.shift, ln.flag)
+    links.epoch = stencil.run_slab(a, b, T, cfg, s.loc_lo, s.gE0, s.out_lo, s.out_hi, lo=side(links.lo),
+                                   hi=side(links.hi), flag=links.flag, epoch=links.epoch, stream=stream)
     return b
-
-
-class _nullctx:
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *exc):
-        return False
 
 
 def connect_fused(slabs, rank: int, bufs, flag, group=None):
@@ -363,38 +332,11 @@ def loopback_fused(stencil, slabs, bufs_per_slab, T: int, cfg: dict, schedule_fn
         links.append(FusedLinks(lo, hi, fptr(k)))
     streams = [torch.cuda.Stream(dev) for _ in range(n)]
     torch.cuda.synchronize(dev)
-    from . import schedule as lib_schedule
-    degrees, trailing = (schedule_fn or lib_schedule)(T, cfg["bT"])
-    # interleave the ranks sweep by sweep (host order only; the flags order the device work)
-    import paper_2001_01473_b200 as an5d
+    # each rank's whole run is enqueued on its own stream, one rank after the other: the stream
+    # waits on the flags order the slabs on the device (a rank blocked in a wait does not hold
+    # the GPU; the others' streams proceed)
     for k, s in enumerate(slabs):
-        a, b = bufs_per_slab[k]
-        stencil.copy_ring(a, b, outer_offset=s.loc_lo, global_outer_extent=s.gE0, stream=streams[k])
-    for i, d in enumerate(degrees):
-        nd = degrees[i + 1] if i + 1 < len(degrees) else 0
-        g = nd * slabs[0].rad
-        for k, s in enumerate(slabs):
-            a, b = bufs_per_slab[k]
-            src, dst = (a, b) if i % 2 == 0 else (b, a)
-            par = (i + 1) % 2
-            ln = links[k]
-            for peer in (ln.lo, ln.hi):
-                if peer is not None:
-                    an5d.stream_wait(peer.flag, i, streams[k])
-            peers = {}
-            if ln.lo is not None and g:
-                peers["lo"] = (ln.lo.bufs[par], ln.lo.shift, g)
-            if ln.hi is not None and g:
-                peers["hi"] = (ln.hi.bufs[par], ln.hi.shift, g)
-            stencil.sweep(src, dst, d, cfg, outer_offset=s.loc_lo, global_outer_extent=s.gE0, out_lo=s.out_lo,
-                          out_hi=s.out_hi, stream=streams[k], peers=peers or None)
-            an5d.stream_signal(ln.flag, i + 1, streams[k])
-    for k, s in enumerate(slabs):
-        if trailing:
-            a, b = bufs_per_slab[k]
-            m = s.out_hi - s.out_lo
-            with torch.cuda.stream(streams[k]):
-                _plane_view(b, s.out_lo, m).copy_(_plane_view(a, s.out_lo, m))
+        run_fused(stencil, s, bufs_per_slab[k], T, cfg, links[k], stream=streams[k])
     torch.cuda.synchronize(dev)
     return [b for _, b in bufs_per_slab]
 
