@@ -66,6 +66,10 @@ CORE_DIRECT = {(2, 0, 1, 2): [(8, 2), (4, 2)]}
 CORE_LAYOUTS = {
     (3, 1, 0, 1): [(2, 3, "t32x2")], (3, 1, 0, 2): [(2, 2, "t32x2")],
     (3, 1, 1, 1): [(2, 2, "t32x2")],
+}
+# fp32 128-wide tiles: measured 5-15 % slower than two 64-wide blocks per SM (r02b suite), never
+# picked by the tuner -> full build only
+FULL_LAYOUTS = {
     (3, 0, 0, 1): [(2, 4, "t32x4")], (3, 0, 0, 2): [(2, 2, "t32x4")], (3, 0, 0, 3): [(2, 1, "t32x4")],
     (3, 0, 0, 4): [(2, 1, "t32x4")], (3, 0, 1, 1): [(2, 2, "t32x4")],
 }
@@ -76,8 +80,8 @@ LAYOUTS = {"": (16, 4), "t32x2": (32, 2), "t32x4": (32, 4)}   # 3D layout -> (TX
 # Measured on B200 (profiles/r02d_split2d.jsonl): 8-13 % SLOWER than one warp per tile for
 # every stencil tried, so the default build keeps only star2d1r (tests, bench --nthr 64) and the
 # full build the rest.
-CORE_SPLIT = {(2, 0, 0, 1): [(8, 8)], (2, 1, 0, 1): [(4, 7)]}
-FULL_SPLIT = {(2, 0, 0, 2): [(8, 6)], (2, 0, 1, 1): [(8, 6)], (2, 1, 0, 2): [(4, 5)]}
+CORE_SPLIT = {(2, 0, 0, 1): [(8, 8)]}
+FULL_SPLIT = {(2, 0, 0, 2): [(8, 6)], (2, 0, 1, 1): [(8, 6)], (2, 1, 0, 1): [(4, 7)], (2, 1, 0, 2): [(4, 5)]}
 
 
 def full_instances():
@@ -135,6 +139,8 @@ def instances():
     if os.environ.get("AN5D_FULL_BUILD", "") not in ("", "0"):
         extra = [(nd, dt, sh, r, bT, v, 1, "w2") for (nd, dt, sh, r), lst in FULL_SPLIT.items()
                  for v, bmax in lst for bT in range(2, bmax + 1)]
+        extra += [(nd, dt, sh, r, bT, v, 1, lay) for (nd, dt, sh, r), lst in FULL_LAYOUTS.items()
+                  for v, bmax, lay in lst for bT in range(1, bmax + 1)]
         out = sorted(set(out) | set(full_instances()) | set(extra))
     dev = os.environ.get("AN5D_DEV_INSTANCES")
     if dev:
