@@ -1044,10 +1044,10 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         const int64_t launches0 = p->launches;
         // one warm-up sweep + two timed sweeps of a configuration: seconds per cell-step (1e300 if
         // it cannot run)
-        // one warm-up sweep, then timed sweeps for >= 8 ms (at least 2, at most 64); every candidate
-        // is timed twice, in opposite orders, and scored by its faster pass: under the 1 kW power
-        // cap the clocks drift by up to 10 % within a tune, which ordered short single passes by
-        // the candidates' position rather than their speed (round-2 measurements)
+        // one warm-up sweep, then timed sweeps for >= 15 ms (at least 2, at most 96); every candidate
+        // is timed in three passes (forward, backward, forward) and scored by its median pass: under
+        // the 1 kW power cap the clocks drift by up to 10 % within a tune, which ordered short
+        // single passes by the candidates' position rather than their speed (round-2 measurements)
         auto measure = [&](const an5d_config& c0, an5d_config& c) -> double {
             if (resolve_config(*p, dm, T, &c0, c) != AN5D_OK) return 1e300;
             auto sweep = [&]() {
@@ -1064,7 +1064,7 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             }
             float ms1 = 0;
             cudaEventElapsedTime(&ms1, e0, e1);
-            const int n = std::max(2, std::min(64, (int)std::ceil(8.0 / std::max(ms1, 1e-3f))));
+            const int n = std::max(2, std::min(96, (int)std::ceil(15.0 / std::max(ms1, 1e-3f))));
             cudaEventRecord(e0, st);
             for (int r = 0; r < n && ok; ++r) ok = sweep();
             cudaEventRecord(e1, st);
@@ -1097,13 +1097,20 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             }
         }
         const bool tlog = getenv("AN5D_TUNE_LOG") != nullptr;   // debug: every candidate's time
+        // three passes (forward, backward, forward), each candidate scored by its median pass
+        std::vector<std::vector<double>> times(cand.size());
         std::vector<double> score(cand.size(), 1e300);
         std::vector<an5d_config> resolved(cand.size());
-        for (int pass = 0; pass < 2; ++pass)
+        for (int pass = 0; pass < 3; ++pass)
             for (size_t j = 0; j < cand.size(); ++j) {
-                const size_t q = pass == 0 ? j : cand.size() - 1 - j;
+                const size_t q = pass == 1 ? cand.size() - 1 - j : j;
                 const double t = measure(cand[q], resolved[q]);
-                score[q] = std::min(score[q], t);
+                times[q].push_back(t);
+                if (times[q].size() == 3) {
+                    std::vector<double> v = times[q];
+                    std::sort(v.begin(), v.end());
+                    score[q] = v[1];
+                }
                 if (tlog)
                     fprintf(stderr, "an5d_tune: pass %d bT %d vec %d n_thr %d bS %d,%d h %lld -> %.4g ps/cell-step\n",
                             pass, cand[q].bT, cand[q].vec, cand[q].n_thr, cand[q].bS[0], cand[q].bS[1],

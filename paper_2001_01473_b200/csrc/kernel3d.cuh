@@ -580,10 +580,12 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 put(dst + st_off);
                 // fused halo exchange: the neighbours' ghost planes, stored straight into their
                 // (peer-mapped) buffers by the same thread (NEXT N1)
+#ifndef AN5D_NO_PEER3D
                 if constexpr (EDGE) {   // units reaching the send bands run the EDGE copy (kernel entry)
                     if (a.peer_lo && p < a.send_lo_end) put(static_cast<T*>(a.peer_lo) + (st_off + a.peer_lo_shift));
                     if (a.peer_hi && p >= a.send_hi_begin) put(static_cast<T*>(a.peer_hi) + (st_off + a.peer_hi_shift));
                 }
+#endif
 #pragma unroll
                 for (int yy = 0; yy < VY; ++yy) {
                     if (a.wc) {
@@ -681,7 +683,7 @@ an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, con
     // the EDGE variant is only for tiles whose window touches the x/y ring or the array end
     if (threadIdx.x == 0) tma_prefetch_desc(&tmap);
     // units storing planes of the fused-exchange send bands run the EDGE copy too
-    if (g.ring_xy || g.p0 < a.send_lo_end || g.p1 > a.send_hi_begin)
+    if (g.ring_xy || (a.peer_lo && g.p0 < a.send_lo_end) || (a.peer_hi && g.p1 > a.send_hi_begin))
         sweep3d_unit<T, R, BT, VY, BOX, true, TXT, VX>(a, cf, smem, g, &tmap);
     else sweep3d_unit<T, R, BT, VY, BOX, false, TXT, VX>(a, cf, smem, g, &tmap);
 }
