@@ -89,3 +89,19 @@ for what in "$@"; do
           python tools/sweeponly.py star2d1r f32 7 45 8 6 32 > gpurun_out/${TAG}_ncu_full.log 2>&1 ;;
   esac
 done
+for what in "$@"; do
+  case $what in
+    peerab)
+      for rep in 1 2 3; do
+        python bench.py --bt 7 --h 45 --nthr 32 --no-tune --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_peerab.jsonl 2>> gpurun_out/${TAG}_suite.err
+        AN5D_LIB=$PWD/paper_2001_01473_b200/libAN5D_nopeer.so python bench.py --bt 7 --h 45 --nthr 32 --no-tune --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_peerab_nopeer.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done
+      for rep in 1 2; do
+        python bench.py --workload box3d2r-f64-512 --bt 1 --h 96 --nthr 256 --no-tune --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_peerab.jsonl 2>> gpurun_out/${TAG}_suite.err
+        AN5D_LIB=$PWD/paper_2001_01473_b200/libAN5D_nopeer.so python bench.py --workload box3d2r-f64-512 --bt 1 --h 96 --nthr 256 --no-tune --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_peerab_nopeer.jsonl 2>> gpurun_out/${TAG}_suite.err
+      done
+      for w in j2d5pt-f32-16384 star2d3r-f32-16384 j2d9pt-f32-16384 star2d1r-f64-16384; do
+        AN5D_TUNE_LOG=1 python bench.py --workload $w --steps 3 --warmup 2 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_tune.jsonl 2>> gpurun_out/${TAG}_tune.err
+      done ;;
+  esac
+done
