@@ -8,6 +8,7 @@ Contents
   * :func:`run` -- the plain double-buffered time loop of PAPER.md fig:jacobi2d with
     Table 2's stencil definitions, in C (oracle.c, OpenMP over the outer dimension),
     fp32 or fp64 arithmetic as the run.
+  * :func:`run_gradient` -- the same loop for the non-linear gradient2d row of Table 2.
   * :mod:`oracle.geometry` -- the paper's blocking bookkeeping formulas
     written out independently of the library's C++ (bit-exact checks of an5d_describe /
     an5d_schedule).
@@ -37,7 +38,7 @@ def build_oracle(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + ".tmp"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
-                               "-shared", _SRC, "-o", tmp])
+                               "-shared", _SRC, "-o", tmp, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -53,6 +54,11 @@ def _load():
             fn.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                            ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_int64, ctypes.c_int]
+        for name in ("oracle_grad_f32", "oracle_grad_f64"):
+            fn = getattr(lib, name)
+            fn.restype = ctypes.c_int
+            fn.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
         lib.oracle_max_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -79,6 +85,25 @@ def run(grid: np.ndarray, rad: int, shape: int, coeffs, divisor: float, T: int, 
     nt = nthreads if nthreads > 0 else lib.oracle_max_threads()
     rc = fn(g.ndim, int(rad), int(shape), c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(divisor), ext,
             g.ctypes.data, out.ctypes.data, int(T), int(nt))
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return out
+
+
+def run_gradient(grid: np.ndarray, centre: float, c0: float, T: int, dtype=np.float32,
+                 nthreads: int = 0) -> np.ndarray:
+    """T steps of gradient2d (Table 2) on a dense 2D grid (ring of width 1
+    included), in ``dtype``: f' = c f + 1 / sqrt(c_0 + sum_{i=-1,+1} ((f - f_{x+i})^2 + (f - f_{y+i})^2)).
+    ``centre`` = c, ``c0`` = c_0, both rounded once to ``dtype``."""
+    lib = _load()
+    g = np.ascontiguousarray(grid, dtype=dtype)
+    if g.ndim != 2:
+        raise ValueError("gradient2d is 2D")
+    out = np.empty_like(g)
+    ext = (ctypes.c_int64 * 2)(*g.shape)
+    fn = lib.oracle_grad_f32 if g.dtype == np.float32 else lib.oracle_grad_f64
+    nt = nthreads if nthreads > 0 else lib.oracle_max_threads()
+    rc = fn(float(centre), float(c0), ext, g.ctypes.data, out.ctypes.data, int(T), int(nt))
     if rc != 0:
         raise ValueError(f"oracle rejected arguments (rc={rc})")
     return out

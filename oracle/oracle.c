@@ -25,6 +25,7 @@
  */
 #include <stdint.h>
 #include <stdlib.h>
+#include <math.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -102,6 +103,53 @@ int NAME(int ndim, int rad, int shape, const double* coeffs, double divisor,    
 
 DEFINE_ORACLE(oracle_run_f32, float)
 DEFINE_ORACLE(oracle_run_f64, double)
+
+/*
+ * gradient2d (Table 2) -- the one non-linear benchmark:
+ *   f'(x,y) = c * f(x,y) + 1.0 / sqrt(c_0 + sum_{i in {-1,+1}} ((f(x,y) - f(x+i,y))^2 + (f(x,y) - f(x,y+i))^2))
+ * with c the centre coefficient and c_0 a constant (both run-time inputs; R-17).  Same
+ * double-buffered loop, ring (rad = 1) never written, arithmetic in the run's dtype, evaluated
+ * left to right as printed: the sum over i = -1 then i = +1, each term (x-difference squared) +
+ * (y-difference squared); then c_0 + sum; IEEE sqrt and IEEE division (no FMA contraction).
+ * Layout: dense row-major, 2D only, extents (E_y, E_x) include the ring.
+ */
+#define DEFINE_GRAD(NAME, T_, SQRT_)                                                             \
+int NAME(double centre, double c0, const int64_t* ext, const T_* in, T_* out, int64_t T,         \
+         int nthreads) {                                                                         \
+    const int64_t ey = ext[0], ex = ext[1];                                                      \
+    if (ey < 3 || ex < 3) return -2;                                                             \
+    const T_ c = (T_)centre, k0 = (T_)c0;                                                        \
+    T_* a = (T_*)malloc(sizeof(T_) * ey * ex);                                                   \
+    T_* b = (T_*)malloc(sizeof(T_) * ey * ex);                                                   \
+    memcpy(a, in, sizeof(T_) * ey * ex);                                                         \
+    memcpy(b, in, sizeof(T_) * ey * ex);                                                         \
+    for (int64_t t = 0; t < T; t++) {                                                            \
+        const T_* src = a;                                                                       \
+        T_* dst = b;                                                                             \
+        _Pragma("omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)")    \
+        for (int64_t y = 1; y < ey - 1; y++) {                                                   \
+            for (int64_t x = 1; x < ex - 1; x++) {                                               \
+                const T_ f = src[y * ex + x];                                                    \
+                T_ sum = (T_)0;                                                                  \
+                for (int i = -1; i <= 1; i += 2) {                                               \
+                    const T_ dx = f - src[y * ex + (x + i)];                                     \
+                    const T_ dy = f - src[(y + i) * ex + x];                                     \
+                    const T_ sx = dx * dx, sy = dy * dy;                                         \
+                    sum = sum + (sx + sy);                                                       \
+                }                                                                                \
+                const T_ cf = c * f;                                                             \
+                dst[y * ex + x] = cf + (T_)1.0 / SQRT_(k0 + sum);                                \
+            }                                                                                    \
+        }                                                                                        \
+        a = dst; b = (T_*)src;                                                                   \
+    }                                                                                            \
+    memcpy(out, a, sizeof(T_) * ey * ex);                                                        \
+    free(a); free(b);                                                                            \
+    return 0;                                                                                    \
+}
+
+DEFINE_GRAD(oracle_grad_f32, float, sqrtf)
+DEFINE_GRAD(oracle_grad_f64, double, sqrt)
 
 int oracle_max_threads(void) {
 #ifdef _OPENMP
