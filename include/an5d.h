@@ -61,7 +61,11 @@ typedef enum {
     AN5D_ERR_OUT_OF_MEMORY = 7
 } an5d_status;
 
-typedef enum { AN5D_STAR = 0, AN5D_BOX = 1 } an5d_shape;  /* P:127-142 */
+/* STAR / BOX: P:127-142.  GRADIENT: the non-linear gradient2d row of Table 2 (P:698-699), 2D,
+ * radius 1 only: f' = c f + 1/sqrt(c_0 + sum_{i=-1,+1} ((f - f(x+i,y))^2 + (f - f(x,y+i))^2)),
+ * c = the table's centre entry (every other entry must be 0), c_0 = an5d_create's `divisor`
+ * argument (not folded); runs on the direct-gather (non-associative) 2D kernel. */
+typedef enum { AN5D_STAR = 0, AN5D_BOX = 1, AN5D_GRADIENT = 2 } an5d_shape;
 typedef enum { AN5D_F32 = 0, AN5D_F64 = 1 } an5d_dtype;   /* P:657-663: single and double */
 
 typedef struct an5d_plan an5d_plan; /* opaque */
@@ -119,6 +123,7 @@ typedef struct {
  *     [-r, r]; entry (d) multiplies the neighbour at offset +d: new[x] = sum_d c_d * old[x+d].
  *     STAR tables must have 0 on every entry with more than one non-zero offset component.
  *   divisor: 1.0 = none; j-stencils (j2d5pt, j2d9pt, j3d27pt) divide the sum by c_0 (Table 2).
+ *     GRADIENT: c_0, the constant under the square root (any finite value, not folded).
  *     Applied as in the paper's fast-math build (P:596-602, P:1019-1021): 1/c_0 is folded into
  *     the coefficients.  Each folded tap is one of the two dtype neighbours of c_d / c_0, chosen
  *     so that the taps' sum is as close as possible to sum_d c_d / c_0 (compensated rounding,

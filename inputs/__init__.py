@@ -27,7 +27,7 @@ import numpy as np
 M32 = 0xFFFFFFFF
 DEFAULT_SEED = 0x200101473
 
-STAR, BOX = 0, 1
+STAR, BOX, GRAD = 0, 1, 2
 
 # PAPER.md Table 2: stencil name -> (ndim, rad, shape, has_divisor)
 # j2d5pt = star2d1r taps / c0; j2d9pt = star2d2r taps / c0 ("2nd-order" P:641-642);
@@ -43,6 +43,8 @@ BENCHMARKS["j2d9pt"] = (2, 2, STAR, True)
 BENCHMARKS["j3d27pt"] = (3, 1, BOX, True)
 # j2d9pt-gol = box2d1r taps / c0 (Table 2, the "game of life"-shaped 9-point Jacobi)
 BENCHMARKS["j2d9pt-gol"] = (2, 1, BOX, True)
+# gradient2d (Table 2): non-linear; "divisor" slot = c_0 under the square root
+BENCHMARKS["gradient2d"] = (2, 1, GRAD, True)
 
 
 def _fmix32(h):
@@ -157,9 +159,23 @@ def coeff_table(ndim: int, rad: int, shape: int, seed: int, kind: str = "dyadic"
     return tab, divisor
 
 
+def gradient_params(seed: int):
+    """gradient2d constants (Table 2 P:698-699 leaves them open): centre c = m / 1024 with
+    m in [256, 768) and c_0 = 1 + m' / 1024 with m' in [0, 1024) -- dyadic (exact in fp32 and
+    fp64).  |c| < 1 and c_0 >= 1 keep a T-step run bounded: f stays in [0, (max f_0) + 1/(1-c)]."""
+    h = hash32(seed + 2, np.array([0, 1]))
+    return 0.25 + float(int(h[0]) % 512) / 1024.0, 1.0 + float(int(h[1]) % 1024) / 1024.0
+
+
 def benchmark_problem(name: str, seed: int = DEFAULT_SEED):
-    """(ndim, rad, shape, coeff_table, divisor) for a Table-2 benchmark with seeded coefficients."""
+    """(ndim, rad, shape, coeff_table, divisor) for a Table-2 benchmark with seeded coefficients.
+    gradient2d: a 3x3 table holding only the centre c, and c_0 in the divisor slot."""
     ndim, rad, shape, has_div = BENCHMARKS[name]
+    if shape == GRAD:
+        c, c0 = gradient_params(seed)
+        tab = np.zeros((3, 3))
+        tab[1, 1] = c
+        return ndim, rad, shape, tab, c0
     tab, div = coeff_table(ndim, rad, shape, seed, kind="int" if has_div else "dyadic")
     return ndim, rad, shape, tab, div
 

@@ -74,8 +74,12 @@ def run(grid: np.ndarray, rad: int, shape: int, coeffs, divisor: float, T: int, 
 
     ``coeffs`` is the dense (2r+1)^ndim table (index order outer..x; entry d multiplies the
     neighbour at offset +d), rounded once to ``dtype``; ``divisor`` divides the sum (IEEE division)
-    when != 1.  ``nthreads`` <= 0 uses all OpenMP threads.
+    when != 1.  ``nthreads`` <= 0 uses all OpenMP threads.  shape 2 = gradient2d: see
+    :func:`run_gradient` (c = the table's centre, c_0 = ``divisor``).
     """
+    if shape == 2:   # gradient2d (Table 2 P:698-699): centre entry of the 3x3 table, c_0 = divisor
+        c = np.asarray(coeffs, dtype=np.float64).reshape(3, 3)
+        return run_gradient(grid, float(c[1, 1]), float(divisor), T, dtype, nthreads)
     lib = _load()
     g = np.ascontiguousarray(grid, dtype=dtype)
     out = np.empty_like(g)

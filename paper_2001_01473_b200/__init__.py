@@ -17,7 +17,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AN5D_LIB") or os.path.join(_HERE, "libAN5D.so")
 
-STAR, BOX = 0, 1
+STAR, BOX, GRAD = 0, 1, 2   # GRAD: gradient2d (Table 2)
 F32, F64 = 0, 1
 
 STATUS = {

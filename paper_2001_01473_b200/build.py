@@ -59,6 +59,8 @@ CORE = {
 }
 # partial sums OFF (direct gather, BASELINE config 4 = box2d2r fp32): vec 8 and 4, b_T 1..2
 CORE_DIRECT = {(2, 0, 1, 2): [(8, 2), (4, 2)]}
+# gradient2d (shape 2, Table 2, NEXT N3): non-linear, direct gather only
+CORE_GRAD = {(2, 0, 2, 1): [(8, 4), (4, 4)], (2, 1, 2, 1): [(4, 3)]}
 # 3D 512-thread layouts (kernel3d.cuh Kernel3DTraits): "t32x2" = 32 x 16 threads with 2-cell patch
 # rows (fp64: 64-wide tiles at half the registers per thread, twice the warps per SM; rad <= 2),
 # "t32x4" = 32 x 16 threads with 4-cell rows (fp32: 128-wide tiles, less x-halo redundancy).
@@ -118,7 +120,7 @@ def full_instances():
 
 def core_instances():
     out = []
-    for tab, assoc in ((CORE, 1), (CORE_DIRECT, 0)):
+    for tab, assoc in ((CORE, 1), (CORE_DIRECT, 0), (CORE_GRAD, 0)):
         for (ndim, dtype, shape, rad), lst in tab.items():
             for vec, bmax in lst:
                 out += [(ndim, dtype, shape, rad, bT, vec, assoc, "") for bT in range(1, bmax + 1)]
@@ -154,7 +156,7 @@ def instances():
 
 
 def inst_name(ndim, dtype, shape, rad, bT, vec, assoc, layout=""):
-    return (f"inst_{ndim}d_{'f64' if dtype else 'f32'}_{'box' if shape else 'star'}_r{rad}"
+    return (f"inst_{ndim}d_{'f64' if dtype else 'f32'}_{('star', 'box', 'grad')[shape]}_r{rad}"
             f"_bt{bT}_v{vec}{'' if assoc else '_direct'}{'_' + layout if layout else ''}")
 
 
@@ -173,7 +175,9 @@ def generate():
         (ndim, dtype, shape, rad, bT, vec, assoc, layout) = inst
         T = "double" if dtype else "float"
         name = inst_name(*inst)
-        targs = f"{T}, {rad}, {bT}, {vec}, {'true' if shape else 'false'}" + ("" if assoc else ", false")
+        targs = f"{T}, {rad}, {bT}, {vec}, {'true' if shape == 1 else 'false'}" + ("" if assoc else ", false")
+        if shape == 2:
+            targs += ", 1, true"   # gradient2d (GRAD template flag)
         if layout == "w2":
             targs += ", true, 2"
         elif layout:

@@ -280,6 +280,9 @@ int resident_blocks(const Instance& inst) {
 int taps_of(const Plan& p) {
     const int w = 2 * p.rad + 1;
     if (p.shape == AN5D_BOX) return p.ndim == 2 ? w * w : w * w * w;
+    // gradient2d: 4 differences, 4 squares, 3 adds, c f + ..., and the IEEE sqrt and division
+    // (each a MUFU seed plus ~8 FMA-pipe refinement ops): ~24 FMA-pipe ops per cell (R-17)
+    if (p.shape == AN5D_GRADIENT) return 24;
     return p.ndim == 2 ? 4 * p.rad + 1 : 6 * p.rad + 1;
 }
 
@@ -435,7 +438,8 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
     const int64_t Iout = dm.E[0] - 2 * p.rad;
     for (const Instance& inst : registry()) {
         if (inst.ndim != p.ndim || inst.shape != p.shape || inst.dtype != p.dtype || inst.rad != p.rad) continue;
-        const int direct = hint ? hint->direct : 0;
+        // gradient2d is non-associative: direct gather only
+        const int direct = p.shape == AN5D_GRADIENT ? 1 : (hint ? hint->direct : 0);
         if (inst.assoc != (direct ? 0 : 1)) continue;
         if (hint && hint->bT && inst.bT != hint->bT) continue;
         if (hint && hint->vec && inst.vec != hint->vec) continue;
@@ -777,6 +781,7 @@ an5d_status check_alignment(const Plan& p, const void* ptr, const Dims& dm, cons
 an5d_status resolve_config(Plan& p, const Dims& dm, int64_t T, const an5d_config* cfg, an5d_config& c) {
     an5d_config hint{};
     if (cfg) hint = *cfg;
+    if (p.shape == AN5D_GRADIENT) hint.direct = 1;   // non-associative: direct gather only
     if (const char* f = getenv("AN5D_FORCE_CFG")) {  // "bT,vec,h" benchmarking override
         int bt = 0, v = 0;
         long long h = 0;
@@ -906,7 +911,10 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
         *out = nullptr;
         if (ndim != 2 && ndim != 3) return fail(AN5D_ERR_INVALID_ARGUMENT, "ndim must be 2 or 3");
         if (radius < 1 || radius > 4) return fail(AN5D_ERR_INVALID_ARGUMENT, "radius must be 1..4");
-        if (shape != AN5D_STAR && shape != AN5D_BOX) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad shape");
+        if (shape != AN5D_STAR && shape != AN5D_BOX && shape != AN5D_GRADIENT)
+            return fail(AN5D_ERR_INVALID_ARGUMENT, "bad shape");
+        if (shape == AN5D_GRADIENT && (ndim != 2 || radius != 1))
+            return fail(AN5D_ERR_UNSUPPORTED, "gradient2d is ndim 2, radius 1 (Table 2 P:698-699)");
         if (dtype != AN5D_F32 && dtype != AN5D_F64) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad dtype");
         if (!coeffs) return fail(AN5D_ERR_INVALID_ARGUMENT, "coeffs is NULL");
         if (!(divisor != 0.0) || !std::isfinite(divisor)) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad divisor");
@@ -920,6 +928,8 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
             if (!std::isfinite(coeffs[k])) return fail(AN5D_ERR_INVALID_ARGUMENT, "non-finite coefficient");
             if (shape == AN5D_STAR && nz > 1 && coeffs[k] != 0.0)
                 return fail(AN5D_ERR_SHAPE_MISMATCH, "STAR table has non-zero off-axis entry %zu", k);
+            if (shape == AN5D_GRADIENT && nz > 0 && coeffs[k] != 0.0)
+                return fail(AN5D_ERR_SHAPE_MISMATCH, "GRADIENT table has non-zero off-centre entry %zu", k);
         }
         an5d_plan* p = new an5d_plan();
         p->ndim = ndim; p->rad = radius; p->shape = shape; p->dtype = dtype;
@@ -927,7 +937,22 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
         p->divisor = divisor;
         p->coeffs_folded.resize(n);
         p->coeffs_dev_t.resize(n * p->elem);
-        if (dtype == AN5D_F32) {
+        if (shape == AN5D_GRADIENT) {
+            // gradient2d: the table rounded once (its centre is c) followed by c_0 = `divisor`,
+            // rounded once; nothing is folded (the divisor is not a divisor here)
+            p->coeffs_dev_t.resize((n + 1) * p->elem);
+            for (size_t k = 0; k <= n; ++k) {
+                const double v = k < n ? coeffs[k] : divisor;
+                if (dtype == AN5D_F32) {
+                    const float f = (float)v;
+                    memcpy(p->coeffs_dev_t.data() + k * 4, &f, 4);
+                    if (k < n) p->coeffs_folded[k] = f;
+                } else {
+                    memcpy(p->coeffs_dev_t.data() + k * 8, &v, 8);
+                    if (k < n) p->coeffs_folded[k] = v;
+                }
+            }
+        } else if (dtype == AN5D_F32) {
             const std::vector<float> f = fold_coefficients<float>(coeffs, n, divisor);
             memcpy(p->coeffs_dev_t.data(), f.data(), n * 4);
             for (size_t k = 0; k < n; ++k) p->coeffs_folded[k] = f[k];

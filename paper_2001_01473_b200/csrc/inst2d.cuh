@@ -6,7 +6,7 @@
 
 namespace an5d {
 
-template <typename T, int R, int BT, int V, bool BOX, bool ASSOC, int NW = 1>
+template <typename T, int R, int BT, int V, bool BOX, bool ASSOC, int NW = 1, bool GRAD = false>
 cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, bool /*edge*/,
                      cudaStream_t st) {
     Coeffs2D<T, R> cf;
@@ -20,8 +20,12 @@ cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, b
         if constexpr (sizeof(T) == 4) cf.c[W * W + dy] = make_float2(c[dy * W + R + 1], c[dy * W + R - 1]);
         else cf.c[W * W + dy] = 0;
     }
+    if constexpr (GRAD) {   // gradient2d: c_0 follows the dense table (an5d_create)
+        if constexpr (sizeof(T) == 4) cf.c[W * W] = make_float2(c[W * W], c[W * W]);
+        else cf.c[W * W] = c[W * W];
+    }
     constexpr size_t smem = smem_bytes_2d<T, R, BT, V, ASSOC, NW>();
-    auto fn = &an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW>;
+    auto fn = &an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW, GRAD>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (smem > 48 * 1024 && !attr_set) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -31,14 +35,14 @@ cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, b
     return cudaGetLastError();
 }
 
-template <typename T, int R, int BT, int V, bool BOX, bool ASSOC = true, int NW = 1>
+template <typename T, int R, int BT, int V, bool BOX, bool ASSOC = true, int NW = 1, bool GRAD = false>
 Instance make_instance2d() {
     Instance i{};
-    i.ndim = 2; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
+    i.ndim = 2; i.shape = GRAD ? 2 : (BOX ? 1 : 0); i.dtype = sizeof(T) == 8 ? 1 : 0;
     i.rad = R; i.bT = BT; i.vec = V; i.assoc = ASSOC ? 1 : 0;
-    i.launch2d = &launch2d<T, R, BT, V, BOX, ASSOC, NW>;
+    i.launch2d = &launch2d<T, R, BT, V, BOX, ASSOC, NW, GRAD>;
     i.launch3d = nullptr;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW>);
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep2d<T, R, BT, V, BOX, ASSOC, NW, GRAD>);
     i.fn_edge = i.fn_interior;
     i.threads = 32 * NW;
     i.tile_x_loaded = 32 * V;

@@ -9,7 +9,7 @@ Pure host arithmetic on counts (no cell data).  Citations:
 """
 from __future__ import annotations
 
-STAR, BOX = 0, 1
+STAR, BOX, GRAD = 0, 1, 2
 
 
 def n_taps(ndim: int, rad: int, shape: int) -> int:
@@ -17,12 +17,19 @@ def n_taps(ndim: int, rad: int, shape: int) -> int:
 
 
 def flops_per_cell(ndim: int, rad: int, shape: int, has_div: bool) -> int:
-    """Table 2: k products summed = k FMA-equivalent ops counted as 2k-1 FLOPs, +1 for /c_0."""
+    """Table 2: k products summed = k FMA-equivalent ops counted as 2k-1 FLOPs, +1 for /c_0;
+    gradient2d: the printed 19."""
+    if shape == GRAD:
+        return 19
     return 2 * n_taps(ndim, rad, shape) - 1 + (1 if has_div else 0)
 
 
 def op_mix(ndim: int, rad: int, shape: int, has_div: bool):
-    """(n_FMA, n_MUL, n_ADD) per cell under the paper's mapping."""
+    """(n_FMA, n_MUL, n_ADD + n_OTHER) per cell under the paper's mapping.
+    gradient2d: 2 FMA (a square added to a square), 3 MUL (two squares, c f),
+    4 differences + 3 adds, and sqrt + division counted as OTHER (R-17)."""
+    if shape == GRAD:
+        return 2, 3, 9
     k = n_taps(ndim, rad, shape)
     return k - 1, 1 + (1 if has_div else 0), 0
 

@@ -115,6 +115,8 @@ def test_exact_integer_bit_identical(an5d, name, dtype):
     GPU result must equal the oracle bit-for-bit whatever the summation order -- pins tile/halo
     indices, boundary masks and the sweep schedule exactly."""
     ndim, rad, shape, _, _ = inputs.benchmark_problem(name)
+    if shape == inputs.GRAD:
+        pytest.skip("gradient2d is not linear; its bit-exact check is test_gradient2d_bit_identical")
     tab, div = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
     ext = small_ext(ndim, rad)
     g = inputs.global_grid(1234, ext, kind="pm")
@@ -126,6 +128,37 @@ def test_exact_integer_bit_identical(an5d, name, dtype):
         got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
         exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
         assert np.array_equal(got, exp), (name, cfg, T)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_gradient2d_bit_identical(an5d, dtype):
+    """gradient2d (Table 2, NEXT N3) on the direct-gather kernel: every operation is
+    individually rounded in the oracle's order (IEEE sqrt and division), so the GPU result equals
+    the oracle BIT FOR BIT at every (b_T, vec), on ragged grids spanning several tiles, for
+    T in {1, b_T, b_T + 1, 2 b_T + 3, 40} -- and every interior cell is stored once per sweep."""
+    ndim, rad, shape, tab, c0 = inputs.benchmark_problem("gradient2d")
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED + 7, ext)
+    st = an5d.Stencil(ndim, rad, shape, tab, c0, dtype)
+    cfgs = configs_for(an5d, st, ext, ndim, direct=1)
+    assert cfgs, "no gradient2d instance"
+    for cfg in cfgs:
+        bT = cfg["bT"]
+        for T in sorted({1, bT, bT + 1, 2 * bT + 3, 40}):
+            got, _ = gpu_run(an5d, ndim, rad, shape, tab, c0, g, T, dtype, cfg)
+            exp = oracle.run(g, rad, shape, tab, c0, T, NP[dtype])
+            assert np.array_equal(got, exp), (cfg, T, rel_linf(got, exp, rad))
+        a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+        b = an5d.empty_grid(ext, rad, dtype)
+        wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+        st.copy_ring(a, b)
+        st.sweep(a, b, bT, cfg, write_count=wc)
+        torch.cuda.synchronize()
+        w = wc.cpu().numpy()
+        core = tuple(slice(rad, e - rad) for e in ext)
+        assert np.all(w[core] == 1), cfg
+        w[core] = 0
+        assert not w.any(), cfg
 
 
 # the default build has direct-gather instances for BASELINE config 4 only (box2d2r fp32); the

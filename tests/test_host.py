@@ -172,6 +172,15 @@ def test_create_rejects_bad_arguments(an5d):
     with pytest.raises(an5d.AN5DError) as e:
         an5d.Stencil(2, 1, an5d.BOX, np.ones((3, 3)), 0.0, torch.float32)
     assert e.value.status == 1
+    # gradient2d (Table 2): 2D radius 1 only, only the centre entry may be non-zero
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.Stencil(2, 2, an5d.GRAD, np.zeros((5, 5)), 1.0, torch.float32)
+    assert e.value.status == 5
+    off = np.zeros((3, 3))
+    off[0, 1] = 0.5
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.Stencil(2, 1, an5d.GRAD, off, 1.0, torch.float32)
+    assert e.value.status == 4
 
 
 def test_flops_per_cell_table2():

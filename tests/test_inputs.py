@@ -31,6 +31,8 @@ def test_torch_generator_matches_numpy():
 
 def test_coeff_tables():
     for name, (ndim, rad, shape, has_div) in inputs.BENCHMARKS.items():
+        if shape == inputs.GRAD:   # centre c and c_0 only (test_benchmark_catalogue_matches_table2)
+            continue
         _, _, _, tab, div = inputs.benchmark_problem(name)
         assert tab.shape == (2 * rad + 1,) * ndim
         nz = np.count_nonzero(tab)
@@ -54,3 +56,6 @@ def test_benchmark_catalogue_matches_table2():
     assert {"j2d5pt", "j2d9pt", "j3d27pt", "j2d9pt-gol"} <= names
     assert inputs.BENCHMARKS["j2d9pt-gol"] == (2, 1, inputs.BOX, True)   # 3x3 box / c_0
     assert inputs.BENCHMARKS["j2d9pt"][1] == 2   # "2nd-order"
+    assert inputs.BENCHMARKS["gradient2d"] == (2, 1, inputs.GRAD, True)
+    ndim, rad, shape, tab, c0 = inputs.benchmark_problem("gradient2d")
+    assert tab.shape == (3, 3) and np.count_nonzero(tab) == 1 and 0 < tab[1, 1] < 1 and c0 >= 1
