@@ -33,7 +33,7 @@ WORKLOADS = {
     "star2d1r-f32-16384": ("star2d1r", "float32", 16384, 1000),
 }
 for _n in ("star2d1r", "star2d2r", "star2d3r", "star2d4r", "box2d1r", "box2d2r", "box2d3r", "box2d4r",
-           "j2d5pt", "j2d9pt", "j2d9pt-gol"):
+           "j2d5pt", "j2d9pt", "j2d9pt-gol", "gradient2d"):
     for _dt in ("f32", "f64"):
         WORKLOADS[f"{_n}-{_dt}-16384"] = (_n, "float32" if _dt == "f32" else "float64", 16384, 1000)
 for _n in ("star3d1r", "star3d2r", "star3d3r", "star3d4r", "box3d1r", "box3d2r", "box3d3r", "box3d4r",
@@ -183,7 +183,10 @@ def cpu_oracle_rate(name, dtype_name, n, host_grid, budget_s=12.0, max_T=None):
 
 def table2_flops_per_cell(ndim, rad, shape, has_div):
     """PAPER.md Table 2 FLOP/cell: k taps -> 2k-1 FLOPs, +1 for the /c_0 of the
-    j-stencils.  Computed here so the reference arm loads nothing from the product package."""
+    j-stencils; gradient2d 19.  Computed here so the reference arm loads nothing from
+    the product package."""
+    if shape == 2:
+        return 19
     k = (2 * rad + 1) ** ndim if shape == 1 else 2 * ndim * rad + 1
     return 2 * k - 1 + (1 if has_div else 0)
 
@@ -255,6 +258,8 @@ def main():
     ap.add_argument("--vec", type=int, default=0)
     ap.add_argument("--h", type=int, default=0)
     ap.add_argument("--nthr", type=int, default=0, help="threads per block of the kernel layout (0 = planner)")
+    ap.add_argument("--bsy", type=int, default=0,
+                    help="3D: loaded tile height b_S_y (32 = one block; 64 / 128 = a cluster of 2 / 4 blocks sharing y halos)")
     ap.add_argument("--direct", type=int, default=0, choices=[0, 1],
                     help="1 = partial sums OFF: the non-associative direct-gather kernels (BASELINE config 4)")
     ap.add_argument("--no-tune", action="store_true", help="planner model only (no measured top-5 pick)")
@@ -328,6 +333,8 @@ def run_an5d(args):
     ext = (n + 2 * rad,) * ndim
     st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
     hint = {"bT": args.bt, "vec": args.vec, "h": args.h, "direct": args.direct, "n_thr": args.nthr}
+    if getattr(args, "bsy", 0):
+        hint["bS"] = [args.bsy, 0]
     a = an5d.empty_grid(ext, rad, dtype, dev)
     b = an5d.empty_grid(ext, rad, dtype, dev)
     fill_uniform(a, inputs.DEFAULT_SEED, ext)

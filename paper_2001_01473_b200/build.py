@@ -65,9 +65,14 @@ CORE_GRAD = {(2, 0, 2, 1): [(8, 4), (4, 4)], (2, 1, 2, 1): [(4, 3)]}
 # rows (fp64: 64-wide tiles at half the registers per thread, twice the warps per SM; rad <= 2),
 # "t32x4" = 32 x 16 threads with 4-cell rows (fp32: 128-wide tiles, less x-halo redundancy).
 # Key as CORE -> [(vec, max b_T, layout)].
+# "c2" / "c4" = the 256-thread layout in thread-block clusters of 2 / 4 blocks stacked along y
+# that share their y halos through DSMEM (NEXT N2; one tile of 64 x 64 / 64 x 128 cells),
+# "c2t32x2" the fp64 512-thread layout in pairs.  rad <= VY (row-band exchange).
 CORE_LAYOUTS = {
-    (3, 1, 0, 1): [(2, 3, "t32x2")], (3, 1, 0, 2): [(2, 2, "t32x2")],
-    (3, 1, 1, 1): [(2, 2, "t32x2")],
+    (3, 1, 0, 1): [(2, 3, "t32x2"), (2, 3, "c2"), (2, 3, "c2t32x2")],
+    (3, 1, 0, 2): [(2, 2, "t32x2"), (2, 2, "c2t32x2")],
+    (3, 1, 1, 1): [(2, 2, "t32x2"), (2, 2, "c2t32x2")],
+    (3, 0, 0, 1): [(2, 4, "c2"), (2, 4, "c4")], (3, 0, 0, 2): [(2, 2, "c2")], (3, 0, 1, 1): [(2, 2, "c2")],
 }
 # fp32 128-wide tiles: measured 5-15 % slower than two 64-wide blocks per SM (r02b suite), never
 # picked by the tuner -> full build only
@@ -75,7 +80,9 @@ FULL_LAYOUTS = {
     (3, 0, 0, 1): [(2, 4, "t32x4")], (3, 0, 0, 2): [(2, 2, "t32x4")], (3, 0, 0, 3): [(2, 1, "t32x4")],
     (3, 0, 0, 4): [(2, 1, "t32x4")], (3, 0, 1, 1): [(2, 2, "t32x4")],
 }
-LAYOUTS = {"": (16, 4), "t32x2": (32, 2), "t32x4": (32, 4)}   # 3D layout -> (TXT, VX)
+# 3D layout -> (TXT, VX, CL): threads along x, cells per thread along x, blocks per cluster along y
+LAYOUTS = {"": (16, 4, 1), "t32x2": (32, 2, 1), "t32x4": (32, 4, 1), "c2": (16, 4, 2), "c4": (16, 4, 4),
+           "c2t32x2": (32, 2, 2)}
 # 2D level split "w2" (kernel2d.cuh Split2D): two warps per tile, warp 0 levels 1..b_T/2 with the
 # staging, warp 1 the rest with the store -- half the partial-sum registers per warp.  b_T 1 has
 # nothing to split: the reduced-degree sweep of degree 1 uses the one-warp instance.
@@ -181,7 +188,7 @@ def generate():
         if layout == "w2":
             targs += ", true, 2"
         elif layout:
-            targs += ", %d, %d" % LAYOUTS[layout]
+            targs += ", %d, %d, %d" % LAYOUTS[layout]
         fn = "make_instance2d" if ndim == 2 else "make_instance3d"
         lines = ["// GENERATED by paper_2001_01473_b200/build.py -- one kernel instance."]
         if name in caps:

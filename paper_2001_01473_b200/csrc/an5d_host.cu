@@ -107,13 +107,15 @@ void make_schedule(int64_t T, int bT, std::vector<int>& deg, bool& trailing_copy
 // Kernel instance for (b_T, vec, direct) with a loaded tile width `tile_x` (0 = any) and
 // `n_thr` threads per block (0 = any).  Among several matches the narrowest tile with the fewest
 // threads is the default (the round-1 layouts), so a config that names neither keeps them.
-const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0, int tile_x = 0, int n_thr = 0) {
+const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0, int tile_x = 0, int n_thr = 0,
+                              int tile_y = 0) {
     const Instance* best = nullptr;
     for (const Instance& i : registry())
         if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad && i.bT == bT &&
             i.vec == vec && i.assoc == (direct ? 0 : 1) && (!tile_x || i.tile_x_loaded == tile_x) &&
-            (!n_thr || i.threads == n_thr))
-            if (!best || std::make_pair(i.tile_x_loaded, i.threads) < std::make_pair(best->tile_x_loaded, best->threads))
+            (!n_thr || i.threads == n_thr) && (!tile_y || i.tile_y == tile_y))
+            if (!best || std::make_tuple(i.tile_x_loaded, i.threads, i.tile_y) <
+                             std::make_tuple(best->tile_x_loaded, best->threads, best->tile_y))
                 best = &i;
     return best;
 }
@@ -127,12 +129,19 @@ int cfg_tile_x(const Plan& p, const an5d_config& c) {
     return bs - 2 * hl + 2 * ((hl + A - 1) / A) * A;
 }
 
+// Loaded y height of a 3D tile a configuration names through b_S_y (0 = not named; 2D: 0).  The y
+// halo is not rounded, so the loaded height is b_S_y itself; it names the cluster layouts (a
+// cluster of CL blocks is one tile of CL x 16 VY rows, NEXT N2).
+int cfg_tile_y(const Plan& p, const an5d_config& c) {
+    return (p.ndim == 3 && c.bT) ? c.bS[0] : 0;
+}
+
 // The instance a sweep of degree d runs under configuration c: the configuration's layout, or for
 // a reduced degree (d < b_T) without that layout (the 2D level split needs d >= 2) the same tile
 // with any thread count -- identical per-cell arithmetic, so the results are the same bits.
 const Instance* find_instance(const Plan& p, int d, const an5d_config& c) {
-    const Instance* i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), c.n_thr);
-    if (!i && d < c.bT) i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), 0);
+    const Instance* i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), c.n_thr, cfg_tile_y(p, c));
+    if (!i && d < c.bT) i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), 0, cfg_tile_y(p, c));
     return i;
 }
 
@@ -277,6 +286,12 @@ int resident_blocks(const Instance& inst) {
     return nblk;
 }
 
+// units resident on the whole GPU: resident blocks x SMs, divided by the blocks one unit takes
+// (a 3D cluster layout runs one unit on CL blocks)
+int64_t resident_units(const Instance& inst) {
+    return std::max<int64_t>(1, (int64_t)resident_blocks(inst) * dev_info().n_sm / std::max(1, inst.cluster));
+}
+
 int taps_of(const Plan& p) {
     const int w = 2 * p.rad + 1;
     if (p.shape == AN5D_BOX) return p.ndim == 2 ? w * w : w * w * w;
@@ -410,7 +425,7 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
     double eta_fma = p.ndim == 2 ? 0.45 : 0.35;
     if (p.ndim == 2 && inst.threads == 64) eta_fma *= 0.88;
     if (p.ndim == 3 && inst.threads == 512) eta_fma *= p.dtype == AN5D_F64 ? 1.25 : 0.87;
-    const double resident = (double)resident_blocks(inst) * di.n_sm;
+    const double resident = (double)resident_units(inst);
     // units are runs of stream blocks (build_runs_2d / _3d); each run pays the overlap once
     double units = (double)g.n_units, unit_rows = (double)rows_per_unit;
     if (run_frac() > 0) {
@@ -445,12 +460,14 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
         if (hint && hint->vec && inst.vec != hint->vec) continue;
         if (hint && hint->n_thr && inst.threads != hint->n_thr) continue;
         if (hint && cfg_tile_x(p, *hint) && inst.tile_x_loaded != cfg_tile_x(p, *hint)) continue;
+        if (hint && cfg_tile_y(p, *hint) && inst.tile_y != cfg_tile_y(p, *hint)) continue;
         if (T > 0 && inst.bT > T) continue;
         // every reduced degree the schedule may need must exist with the same tile
+        const int ty = p.ndim == 3 ? inst.tile_y : 0;
         bool ok = true;
         for (int d = 1; d < inst.bT && ok; ++d)
-            ok = find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, inst.threads) != nullptr ||
-                 find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, 0) != nullptr;
+            ok = find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, inst.threads, ty) != nullptr ||
+                 find_instance(p, d, inst.vec, direct, inst.tile_x_loaded, 0, ty) != nullptr;
         if (!ok) continue;
         std::vector<int64_t> hs;
         if (hint && hint->h) {
@@ -460,7 +477,7 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
             if (sweep_geometry(p, inst, dm, inst.bT, Iout, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g) != AN5D_OK) continue;
             int64_t nt = 1;
             for (int i = 0; i < p.ndim - 1; ++i) nt *= g.ntiles[i];
-            const int64_t conc = (int64_t)resident_blocks(inst) * di.n_sm;
+            const int64_t conc = resident_units(inst);
             // stream-block lengths giving 1..32 units per resident block, and a few fixed lengths
             for (int w : {1, 2, 4, 8, 16, 32}) {
                 const int64_t nsb = std::max<int64_t>(1, (w * conc) / std::max<int64_t>(1, nt));
@@ -601,7 +618,8 @@ an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src,
     x_off = (int)((base - aligned) / p.elem);
     const cuuint64_t dims[3] = {(cuuint64_t)(dm.E[2] + x_off), (cuuint64_t)dm.E[1], (cuuint64_t)dm.E[0]};
     const cuuint64_t strides[2] = {(cuuint64_t)(dm.pitch[1] * p.elem), (cuuint64_t)(dm.pitch[0] * p.elem)};
-    const cuuint32_t box[3] = {(cuuint32_t)inst.tile_x_loaded, (cuuint32_t)inst.tile_y, 1};
+    // one block's plane: a cluster layout's blocks each load their own tile_y / cluster rows
+    const cuuint32_t box[3] = {(cuuint32_t)inst.tile_x_loaded, (cuuint32_t)(inst.tile_y / std::max(1, inst.cluster)), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(&tm, p.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                         reinterpret_cast<void*>(aligned), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -710,7 +728,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         set_peers(a, peers, dm.pitch[0], out_lo, out_hi);
         const double frac = run_frac();
         if (frac > 0) {
-            const int64_t W = run_warps((int64_t)resident_blocks(*inst) * dev_info().n_sm);
+            const int64_t W = run_warps(resident_units(*inst));
             const std::vector<int64_t> key = {3, d, g.ntiles[0], g.ntiles[1], g.n_sb, g.sb_lo, g.sb_hi, W,
                                               (int64_t)(frac * 1e6)};
             auto it = p.runs.find(key);
@@ -1036,7 +1054,9 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         // layouts only roughly (measured on B200: the 2D level split ranks high in the model and
         // runs 8-20 % slower; the 512-thread fp64 3D layout runs 15-30 % faster), so every layout
         // is measured rather than ranked.
-        auto layout_of = [&](const an5d_config& c) { return std::make_tuple(c.vec, c.n_thr, cfg_tile_x(*p, c)); };
+        auto layout_of = [&](const an5d_config& c) {
+            return std::make_tuple(c.vec, c.n_thr, cfg_tile_x(*p, c), cfg_tile_y(*p, c));
+        };
         std::vector<std::pair<int, int>> pairs;
         for (const auto& r : ranked) {
             const std::pair<int, int> bv(r.second.bT, r.second.vec);
@@ -1217,11 +1237,10 @@ an5d_status an5d_describe(an5d_plan* p, const int64_t* extents, const an5d_confi
                                         : g.n_units;
         out->n_units = run_frac() > 0
                            ? (int64_t)build_runs(p->ndim, g,
-                                                 run_warps(p->ndim == 2 ? out->grid_blocks
-                                                                        : (int64_t)resident_blocks(*inst) * dev_info().n_sm),
+                                                 run_warps(p->ndim == 2 ? out->grid_blocks : resident_units(*inst)),
                                                  run_frac()).size()
                            : g.n_units;
-        if (p->ndim == 3) out->grid_blocks = out->n_units;
+        if (p->ndim == 3) out->grid_blocks = out->n_units * std::max(1, inst->cluster);
         out->smem_bytes = inst->smem_bytes;
         cudaFuncAttributes attr{};
         if (cudaFuncGetAttributes(&attr, inst->fn_interior) == cudaSuccess) out->regs_per_thread = attr.numRegs;

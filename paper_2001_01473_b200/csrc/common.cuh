@@ -133,6 +133,26 @@ __device__ __forceinline__ void tma_load_3d(void* sdst, const void* tmap, int c0
                  "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
                  : "memory");
 }
+// ---- thread-block clusters (DSMEM) -------------------------------------------------------------
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+// barrier over every thread of the cluster; release/acquire at cluster scope orders the shared
+// memory writes before it with the (local or remote) reads after it
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// generic address of the same shared-memory location in CTA `rank` of the cluster (DSMEM):
+// ordinary loads through it read the peer's shared memory
+template <typename T>
+__device__ __forceinline__ const T* map_cta(const T* p, unsigned rank) {
+    uint64_t out;
+    asm volatile("mapa.u64 %0, %1, %2;\n" : "=l"(out) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+    return reinterpret_cast<const T*>(out);
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }

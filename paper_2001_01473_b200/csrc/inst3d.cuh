@@ -6,7 +6,7 @@
 
 namespace an5d {
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX, int CL = 1>
 cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap& tmap, int64_t blocks,
                      cudaStream_t st) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
@@ -22,29 +22,48 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
         if constexpr (sizeof(T) == 4) cf.c[N + r] = make_float2(c[r * W + R + 1], c[r * W + R - 1]);
         else cf.c[N + r] = 0;
     }
-    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX>;
+    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (!attr_set) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
         attr_set = true;
     }
-    fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf, tmap);
+    if constexpr (CL == 1) {
+        fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf, tmap);
+    } else {
+        // one cluster of CL blocks per unit (NEXT N2: cluster halo sharing along y)
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3((unsigned)(blocks * CL), 1, 1);
+        lc.blockDim = dim3(K::kThreads, 1, 1);
+        lc.dynamicSmemBytes = K::kSmemBytes;
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&lc, fn, a, cf, tmap);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1>
 Instance make_instance3d() {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
     Instance i{};
     i.ndim = 3; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
     i.rad = R; i.bT = BT; i.vec = VY; i.assoc = 1;
     i.launch2d = nullptr;
-    i.launch3d = &launch3d<T, R, BT, VY, BOX, TXT, VX>;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX>);
+    i.launch3d = &launch3d<T, R, BT, VY, BOX, TXT, VX, CL>;
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL>);
     i.fn_edge = i.fn_interior;
     i.threads = K::kThreads;
     i.tile_x_loaded = K::kTX;
-    i.tile_y = K::kTY;
+    i.tile_y = K::kTY * CL;    // a cluster's blocks form one tile of CL x kTY rows
+    i.cluster = CL;
     i.smem_bytes = K::kSmemBytes;
     return i;
 }

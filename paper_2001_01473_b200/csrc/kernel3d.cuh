@@ -138,10 +138,25 @@ using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * 
 // the mixed pair (c[dz][dy][+1], c[dz][dy][-1]) for the swapped-operand FFMA2 of the dx = +-1
 // taps (see kernel2d.cuh Coeffs2D).
 
-template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_>
+// CL > 1 (NEXT N2, thread-block-cluster halo sharing): the CL thread blocks of a cluster stack
+// their tile windows along y and form ONE tall tile of CL x kTY rows: the y halo of b_T rad rows is
+// loaded and recomputed only at the cluster's outer rows.  At a block's inner boundary the rows
+// the neighbour owns come from the neighbour's shared memory (DSMEM): level 1 from its staged
+// plane, level L >= 2 from its exchange buffer; the per-step block barrier becomes a cluster
+// barrier (release/acquire), which also orders the neighbour's reads against the reuse of its
+// stage slots and exchange buffers (both are double-buffered or D - PF >= 1 planes deep).
+template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_, int CL = 1>
 __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
-                                             const Unit3D& g, const void* tmap) {
+                                             const Unit3D& g, const void* tmap, const unsigned crank = 0) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX_>;
+    static_assert(CL == 1 || !K::XPLANE, "cluster halo sharing needs rad <= VY (row-band exchange)");
+    // block barrier (CL = 1) or cluster barrier (CL > 1)
+    auto block_sync = [&]() {
+        if constexpr (CL > 1) cluster_sync_all();
+        else __syncthreads();
+    };
+    [[maybe_unused]] const bool peer_up = CL > 1 && crank > 0;          // block above in the cluster
+    [[maybe_unused]] const bool peer_dn = CL > 1 && crank + 1 < (unsigned)CL;   // block below
     using LN = Lane<T, K::VX>;
     using E = typename LN::E;
     constexpr int NE = LN::NE;              // elements per patch row
@@ -237,6 +252,10 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
         for (int j = 0; j < NCH; ++j) st_vec_shared<T>(p + j * A, c + j * A);
     };
+    // a patch row of a neighbour block of the cluster: the same shared-memory offset in CTA `rank`
+    [[maybe_unused]] auto load_row_peer = [&](E (&P_)[NE], const T* p, unsigned rank) {
+        load_row(P_, map_cta(p, rank));
+    };
 
     // ---- register state ---------------------------------------------------------------------------
     E acc[BT][P][VY][NE];
@@ -301,8 +320,16 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if constexpr (!K::XPLANE) {
-                load_row(lo[r], xw + tyi * K::XBAND + (R + r) * kTX + xs);         // above: its bottom rows
-                load_row(hi[r], xw + (tyi + 2) * K::XBAND + r * kTX + xs);         // below: its top rows
+                // cluster: the top thread row's "above" is the bottom thread row (band TYT) of the
+                // block above, the bottom thread row's "below" the top thread row (band 1) below
+                if (CL > 1 && tyi == 0 && peer_up)
+                    load_row_peer(lo[r], xw + K::TYT * K::XBAND + (R + r) * kTX + xs, crank - 1);
+                else
+                    load_row(lo[r], xw + tyi * K::XBAND + (R + r) * kTX + xs);     // above: its bottom rows
+                if (CL > 1 && tyi == K::TYT - 1 && peer_dn)
+                    load_row_peer(hi[r], xw + 1 * K::XBAND + r * kTX + xs, crank + 1);
+                else
+                    load_row(hi[r], xw + (tyi + 2) * K::XBAND + r * kTX + xs);     // below: its top rows
             } else {
                 load_row(lo[r], xw + own + (r - R) * kTX);
                 load_row(hi[r], xw + own + (VY + r) * kTX);
@@ -323,7 +350,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             const int64_t s = base + k;
             const int si = i;
             wait_plane(slot_i);                                // plane s has landed (TMA, mbarrier)
-            __syncthreads();                                   // ... and every thread is past step s-1
+            block_sync();                                      // ... and every thread (of the cluster) is past step s-1
             {
                 int ns = slot_i + PF;
                 if (ns >= D) ns -= D;
@@ -353,8 +380,16 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                     for (int yy = 0; yy < VY; ++yy) load_row(u0[yy], cur + own + yy * kTX);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        load_row(yh_lo[r], cur + own + (r - R) * kTX);
-                        load_row(yh_hi[r], cur + own + (VY + r) * kTX);
+                        // cluster: rows owned by the block above / below come from its staged plane
+                        // (same slot: both blocks stream the same planes in lockstep)
+                        if (CL > 1 && tyi == 0 && peer_up)
+                            load_row_peer(yh_lo[r], cur + (K::kTY + r) * kTX + xs, crank - 1);
+                        else
+                            load_row(yh_lo[r], cur + own + (r - R) * kTX);
+                        if (CL > 1 && tyi == K::TYT - 1 && peer_dn)
+                            load_row_peer(yh_hi[r], cur + (R + r) * kTX + xs, crank + 1);
+                        else
+                            load_row(yh_hi[r], cur + own + (VY + r) * kTX);
                     }
                 } else if constexpr (SK) {
                     // halo rows of level L-1's plane of the previous step, exchanged at its end
@@ -365,7 +400,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                     T* xw = xch + (size_t)xb * K::XBUF;
                     xb ^= 1;
                     publish(xw, u);
-                    __syncthreads();
+                    block_sync();
                     read_halo(xw, yh_lo, yh_hi);
                 }
                 // x halo of a row: rad cells from the left / right thread of the 16-lane segment
@@ -627,6 +662,8 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
         wait_plane(slot_i);
         if (++slot_i == D) slot_i = 0;
     }
+    // cluster: no block may exit (releasing its shared memory) while a neighbour can still read it
+    if constexpr (CL > 1) cluster_sync_all();
 }
 
 // resident blocks per SM the register budget is shaped for: small fp32 patches (VY <= 2) fit two
@@ -643,14 +680,17 @@ template <typename T, int VY, int R, bool BOX, int TXT> constexpr int min_blocks
 #endif
 }
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4>
+// CL > 1: launched with cluster dimension (CL, 1, 1); the CL consecutive blocks of a cluster take
+// the same unit (a cluster tile of CL x kTY rows) and block rank c its rows [c kTY, (c+1) kTY).
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1>
 __global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
 an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* const smem = reinterpret_cast<T*>(smem_raw);
-    const int64_t unit = blockIdx.x;
-    if (unit >= a.n_units) return;
+    const int64_t unit = blockIdx.x / CL;
+    const unsigned crank = CL > 1 ? cluster_ctarank() : 0;
+    if (unit >= a.n_units) return;   // the whole cluster (same unit) leaves together
     int ty, tx;
     int64_t sb, sb_end;
     if (a.runs) {
@@ -666,11 +706,14 @@ an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, con
         sb_end = sb + 1;
     }
     Unit3D g;
-    g.cy0 = R + ty * a.Cy;
-    g.cy1 = min(g.cy0 + a.Cy, a.Ey - R);
+    {   // compute rows of the (cluster) tile, then this block's window and its share of them
+        const int cy0 = R + ty * a.Cy, cy1 = min(cy0 + a.Cy, a.Ey - R);
+        g.wy0 = cy0 - a.Hy + (int)crank * K::kTY;
+        g.cy0 = max(cy0, g.wy0);
+        g.cy1 = min(cy1, g.wy0 + K::kTY);   // may be empty (a block below the array end)
+    }
     g.cx0 = R + tx * a.Cx;
     g.cx1 = min(g.cx0 + a.Cx, a.Ex - R);
-    g.wy0 = g.cy0 - a.Hy;
     g.wx0 = g.cx0 - a.Hx;
     g.p0 = a.out_lo + sb * a.h;
     g.p1 = min(a.out_lo + sb_end * a.h, a.out_hi);
@@ -684,8 +727,8 @@ an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, con
     if (threadIdx.x == 0) tma_prefetch_desc(&tmap);
     // units storing planes of the fused-exchange send bands run the EDGE copy too
     if (g.ring_xy || (a.peer_lo && g.p0 < a.send_lo_end) || (a.peer_hi && g.p1 > a.send_hi_begin))
-        sweep3d_unit<T, R, BT, VY, BOX, true, TXT, VX>(a, cf, smem, g, &tmap);
-    else sweep3d_unit<T, R, BT, VY, BOX, false, TXT, VX>(a, cf, smem, g, &tmap);
+        sweep3d_unit<T, R, BT, VY, BOX, true, TXT, VX, CL>(a, cf, smem, g, &tmap, crank);
+    else sweep3d_unit<T, R, BT, VY, BOX, false, TXT, VX, CL>(a, cf, smem, g, &tmap, crank);
 }
 
 }  // namespace an5d

@@ -28,6 +28,7 @@ struct Instance {
     int tile_x_loaded;                       // cells per tile along x (loaded window)
     int tile_y;                              // 3D: cells per tile along y; 2D: 0
     size_t smem_bytes;                       // dynamic shared memory per block
+    int cluster;                             // 3D: blocks per cluster along y (tile_y = cluster x block rows)
 };
 
 std::vector<Instance>& registry();

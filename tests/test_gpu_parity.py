@@ -161,6 +161,53 @@ def test_gradient2d_bit_identical(an5d, dtype):
         assert not w.any(), cfg
 
 
+CLUSTER_CASES = [("star3d1r", torch.float32, 4, 256, (2, 4)), ("star3d2r", torch.float32, 2, 256, (2,)),
+                 ("box3d1r", torch.float32, 2, 256, (2,)), ("j3d27pt", torch.float32, 2, 256, (2,)),
+                 ("star3d1r", torch.float64, 3, 256, (2,)), ("star3d1r", torch.float64, 3, 512, (2,)),
+                 ("star3d2r", torch.float64, 2, 512, (2,)), ("box3d1r", torch.float64, 2, 512, (2,))]
+
+
+@pytest.mark.parametrize("name,dtype,bmax,n_thr,cls", CLUSTER_CASES)
+def test_cluster_halo_sharing(an5d, name, dtype, bmax, n_thr, cls):
+    """3D thread-block clusters (NEXT N2): CL blocks stacked along y share their y halos through
+    DSMEM -- one tile of CL x 32 rows.  Per cell the arithmetic is unchanged, so every run is
+    BIT-IDENTICAL to the one-block layout (32-row tiles) with the same b_T, matches the oracle
+    within tolerance on random inputs and bit-for-bit in exact-integer mode, and stores every
+    interior cell once per sweep (ragged grids: several cluster tiles in y, partial last one)."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    gx = inputs.global_grid(1234, ext, kind="pm")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    for cl in cls:
+        for bT in range(1, bmax + 1):
+            cfg = {"bT": bT, "vec": 2, "h": 8, "n_thr": n_thr, "bS": [32 * cl, 0]}
+            d = st.describe(ext, cfg)
+            assert d["bS_loaded"][0] == 32 * cl and d["grid_blocks"] % cl == 0, d
+            ref_cfg = dict(cfg, bS=[32, 0])
+            for T in sorted({1, bT, 2 * bT + 3}):
+                got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+                ref, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, ref_cfg)
+                assert np.array_equal(got, ref), (name, cl, bT, T)
+                exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+                assert ring_equal(got, exp, rad) and rel_linf(got, exp, rad) <= TOL[dtype], (name, cl, bT, T)
+            T = _exact_T(ndim, rad, shape, 2 * bT + 3, dtype)
+            got, _ = gpu_run(an5d, ndim, rad, shape, tabx, divx, gx, T, dtype, cfg)
+            assert np.array_equal(got, oracle.run(gx, rad, shape, tabx, divx, T, NP[dtype])), (name, cl, bT, T)
+            a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+            b = an5d.empty_grid(ext, rad, dtype)
+            wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+            st.copy_ring(a, b)
+            st.sweep(a, b, bT, cfg, write_count=wc)
+            torch.cuda.synchronize()
+            w = wc.cpu().numpy()
+            core = tuple(slice(rad, e - rad) for e in ext)
+            assert np.all(w[core] == 1), (cl, bT)
+            w[core] = 0
+            assert not w.any(), (cl, bT)
+
+
 # the default build has direct-gather instances for BASELINE config 4 only (box2d2r fp32); the
 # full build (AN5D_FULL_BUILD=1) adds box2d1r-4r fp32/fp64, which this test then also covers
 @pytest.mark.parametrize("name,dtype", [("box2d2r", torch.float32)] + [
