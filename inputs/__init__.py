@@ -159,6 +159,59 @@ def coeff_table(ndim: int, rad: int, shape: int, seed: int, kind: str = "dyadic"
     return tab, divisor
 
 
+# Multi-field systems (NEXT N4, "multi-output temporal blocking ... multi-statement
+# stencils"): name -> (ndim, rad, shape, n_fields).  n_f arrays updated together, statement i
+# reading the previous step of every array through a Table-2-shaped block (i, j).
+SYSTEMS = {
+    "star2d1r-x2": (2, 1, STAR, 2),
+    "box2d1r-x2": (2, 1, BOX, 2),
+}
+
+
+def system_table(ndim: int, rad: int, shape: int, nf: int, seed: int, kind: str = "dyadic"):
+    """(n_f, n_f, (2r+1,)*ndim) float64 block table; block [i, j] = field j's contribution to field i.
+
+    kind='dyadic': integer weights m in [1, 1024] on every tap of every block, the diagonal block's
+    centre raised so that each OUTPUT field's weights sum to 2^p, divided by 2^p: every statement
+    sums to 1 exactly (a constant state is a fixed point; values stay in [0, 1]).
+    kind='pm1': +-1 per tap (exact-integer mode)."""
+    w = 2 * rad + 1
+    tab = np.zeros((nf, nf) + (w,) * ndim, dtype=np.float64)
+    offs = tap_offsets(ndim, rad, shape)
+    centre = tuple(rad for _ in range(ndim))
+    for i in range(nf):
+        for j in range(nf):
+            for d in offs:
+                lin = ((i * nf + j) * w ** ndim + sum((v + rad) * w ** (ndim - 1 - a) for a, v in enumerate(d)))
+                h = int(hash32(seed + 3, np.array([lin]))[0])
+                if kind == "pm1":
+                    m = 1.0 if h & 1 else -1.0
+                else:
+                    m = float(1 + h % 1024)
+                tab[(i, j) + tuple(v + rad for v in d)] = m
+        if kind == "dyadic":
+            s_other = tab[i].sum() - tab[(i, i) + centre]
+            p = 0
+            while (1 << p) <= s_other:
+                p += 1
+            tab[(i, i) + centre] = float((1 << p) - s_other)
+            tab[i] /= float(1 << p)
+        elif kind != "pm1":
+            raise ValueError(kind)
+    return tab
+
+
+def system_problem(name: str, seed: int = DEFAULT_SEED):
+    """(ndim, rad, shape, n_fields, block table) of a catalogued multi-field system."""
+    ndim, rad, shape, nf = SYSTEMS[name]
+    return ndim, rad, shape, nf, system_table(ndim, rad, shape, nf, seed)
+
+
+def system_fields(seed: int, nf: int, extents, kind: str = "uniform") -> np.ndarray:
+    """(n_f, *extents) float64 seeded fields: field f uses seed + 0x1000 * f."""
+    return np.stack([global_grid(seed + 0x1000 * f, extents, kind=kind) for f in range(nf)])
+
+
 def gradient_params(seed: int):
     """gradient2d constants (Table 2 P:698-699 leaves them open): centre c = m / 1024 with
     m in [256, 768) and c_0 = 1 + m' / 1024 with m' in [0, 1024) -- dyadic (exact in fp32 and

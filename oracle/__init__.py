@@ -9,6 +9,8 @@ Contents
     Table 2's stencil definitions, in C (oracle.c, OpenMP over the outer dimension),
     fp32 or fp64 arithmetic as the run.
   * :func:`run_gradient` -- the same loop for the non-linear gradient2d row of Table 2.
+  * :func:`run_system` -- the same loop for a system of n_f arrays updated together, every
+    statement reading the previous step of all arrays (NEXT N4).
   * :mod:`oracle.geometry` -- the paper's blocking bookkeeping formulas
     written out independently of the library's C++ (bit-exact checks of an5d_describe /
     an5d_schedule).
@@ -54,6 +56,12 @@ def _load():
             fn.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                            ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_int64, ctypes.c_int]
+        for name in ("oracle_system_f32", "oracle_system_f64"):
+            fn = getattr(lib, name)
+            fn.restype = ctypes.c_int
+            fn.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                           ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                           ctypes.c_int]
         for name in ("oracle_grad_f32", "oracle_grad_f64"):
             fn = getattr(lib, name)
             fn.restype = ctypes.c_int
@@ -108,6 +116,31 @@ def run_gradient(grid: np.ndarray, centre: float, c0: float, T: int, dtype=np.fl
     fn = lib.oracle_grad_f32 if g.dtype == np.float32 else lib.oracle_grad_f64
     nt = nthreads if nthreads > 0 else lib.oracle_max_threads()
     rc = fn(float(centre), float(c0), ext, g.ctypes.data, out.ctypes.data, int(T), int(nt))
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return out
+
+
+def run_system(fields: np.ndarray, rad: int, shape: int, coeffs, T: int, dtype=np.float32,
+               nthreads: int = 0) -> np.ndarray:
+    """T steps of a multi-field system (NEXT N4) on ``fields`` of shape (n_f, *grid) (rings
+    included): A_i' = sum_j sum_d c[i, j][d] A_j[x + d] over the Table-2 taps of ``shape``.
+    ``coeffs``: shape (n_f, n_f, (2r+1,)*ndim); block [i, j] is field j's contribution to field i,
+    rounded once to ``dtype``.  Returns a new (n_f, *grid) array."""
+    lib = _load()
+    f = np.ascontiguousarray(fields, dtype=dtype)
+    nf = f.shape[0]
+    grid = f.shape[1:]
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64))
+    if c.shape[:2] != (nf, nf):
+        raise ValueError("coeffs must be (n_f, n_f, table)")
+    c = c.reshape(-1)
+    out = np.empty_like(f)
+    ext = (ctypes.c_int64 * len(grid))(*grid)
+    fn = lib.oracle_system_f32 if f.dtype == np.float32 else lib.oracle_system_f64
+    nt = nthreads if nthreads > 0 else lib.oracle_max_threads()
+    rc = fn(len(grid), int(rad), int(shape), int(nf), c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ext,
+            f.ctypes.data, out.ctypes.data, int(T), int(nt))
     if rc != 0:
         raise ValueError(f"oracle rejected arguments (rc={rc})")
     return out

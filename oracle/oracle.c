@@ -151,6 +151,78 @@ int NAME(double centre, double c0, const int64_t* ext, const T_* in, T_* out, in
 DEFINE_GRAD(oracle_grad_f32, float, sqrtf)
 DEFINE_GRAD(oracle_grad_f64, double, sqrt)
 
+/*
+ * Multi-field systems (NEXT N4, "multi-output temporal blocking to optimize multi-statement
+ * stencils"): n_f arrays updated together, one statement per array, every statement
+ * reading the previous time step of all arrays (Jacobi in time, like fig:jacobi2d P:406-413):
+ *   for t in 0..T-1, for every field i, for every interior cell x:
+ *       A_i[(t+1)%2][x] = sum_{j=0..n_f-1} sum_{d in taps} c_{ij,d} * A_j[t%2][x+d]
+ * Table 2 shapes per (i, j) block (star or box), taps in lexicographic order, the j
+ * sum outermost, in the run's dtype with separate multiply and add (built -ffp-contract=off).
+ * Layout: fields are consecutive dense arrays (field f at f * prod(ext)); coeffs: n_f * n_f dense
+ * (2r+1)^ndim tables, block (i, j) at (i * n_f + j) * (2r+1)^ndim (contribution of field j to
+ * field i).  The ring of width rad of every field is never written.
+ */
+#define DEFINE_SYSTEM(NAME, T_)                                                                  \
+int NAME(int ndim, int rad, int shape, int nf, const double* coeffs, const int64_t* ext,        \
+         const T_* in, T_* out, int64_t T, int nthreads) {                                       \
+    if (ndim < 1 || ndim > 3 || rad < 1 || nf < 1 || nf > 8) return -1;                         \
+    int64_t ncell = 1;                                                                           \
+    for (int i = 0; i < ndim; i++) { if (ext[i] < 2 * rad + 1) return -2; ncell *= ext[i]; }     \
+    int w = 2 * rad + 1, n_dense = 1;                                                            \
+    for (int i = 0; i < ndim; i++) n_dense *= w;                                                 \
+    int64_t* lin_off = (int64_t*)malloc(sizeof(int64_t) * n_dense);                              \
+    double* cd = (double*)malloc(sizeof(double) * n_dense);                                      \
+    T_* c = (T_*)malloc(sizeof(T_) * n_dense * nf * nf);                                         \
+    int ntap = 0;                                                                                \
+    for (int b = 0; b < nf * nf; b++) {                                                          \
+        ntap = build_taps(ndim, rad, shape, coeffs + (int64_t)b * n_dense, ext, lin_off, cd);    \
+        for (int k = 0; k < ntap; k++) c[b * n_dense + k] = (T_)cd[k];                           \
+    }                                                                                            \
+    T_* a = (T_*)malloc(sizeof(T_) * ncell * nf);                                                \
+    T_* bb = (T_*)malloc(sizeof(T_) * ncell * nf);                                               \
+    memcpy(a, in, sizeof(T_) * ncell * nf);                                                      \
+    memcpy(bb, in, sizeof(T_) * ncell * nf); /* rings of the second buffers = input rings */     \
+    int64_t e0 = ndim >= 3 ? ext[ndim - 3] : 1;                                                  \
+    int64_t e1 = ndim >= 2 ? ext[ndim - 2] : 1;                                                  \
+    int64_t e2 = ext[ndim - 1];                                                                  \
+    int64_t lo0 = ndim >= 3 ? rad : 0, hi0 = ndim >= 3 ? e0 - rad : 1;                          \
+    int64_t lo1 = ndim >= 2 ? rad : 0, hi1 = ndim >= 2 ? e1 - rad : 1;                           \
+    int64_t lo2 = rad, hi2 = e2 - rad;                                                           \
+    for (int64_t t = 0; t < T; t++) {                                                            \
+        const T_* src = a;                                                                       \
+        T_* dst = bb;                                                                            \
+        int64_t nouter = (hi0 - lo0) * (hi1 - lo1);                                              \
+        for (int fi = 0; fi < nf; fi++) {                                                        \
+            _Pragma("omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)") \
+            for (int64_t o = 0; o < nouter; o++) {                                               \
+                int64_t i0 = lo0 + o / (hi1 - lo1), i1 = lo1 + o % (hi1 - lo1);                  \
+                int64_t rowbase = (i0 * e1 + i1) * e2;                                           \
+                for (int64_t i2 = lo2; i2 < hi2; i2++) {                                         \
+                    int64_t x = rowbase + i2;                                                    \
+                    T_ acc = (T_)0;                                                              \
+                    for (int fj = 0; fj < nf; fj++) {                                            \
+                        const T_* s = src + (int64_t)fj * ncell;                                 \
+                        const T_* cb = c + (int64_t)(fi * nf + fj) * n_dense;                    \
+                        for (int k = 0; k < ntap; k++) {                                         \
+                            T_ prod = cb[k] * s[x + lin_off[k]];                                 \
+                            acc = acc + prod;                                                    \
+                        }                                                                        \
+                    }                                                                            \
+                    dst[(int64_t)fi * ncell + x] = acc;                                          \
+                }                                                                                \
+            }                                                                                    \
+        }                                                                                        \
+        a = dst; bb = (T_*)src;                                                                  \
+    }                                                                                            \
+    memcpy(out, a, sizeof(T_) * ncell * nf);                                                     \
+    free(a); free(bb); free(lin_off); free(cd); free(c);                                         \
+    return 0;                                                                                    \
+}
+
+DEFINE_SYSTEM(oracle_system_f32, float)
+DEFINE_SYSTEM(oracle_system_f64, double)
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
