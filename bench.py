@@ -41,6 +41,10 @@ for _n in ("star3d1r", "star3d2r", "star3d3r", "star3d4r", "box3d1r", "box3d2r",
     for _dt in ("f32", "f64"):
         WORKLOADS[f"{_n}-{_dt}-512"] = (_n, "float32" if _dt == "f32" else "float64", 512, 1000)
 WORKLOADS["star3d2r-f32-1536"] = ("star3d2r", "float32", 1536, 1000)
+# multi-field systems (NEXT N4): GCells/s counts cells of every field
+for _n in ("star2d1r-x2", "box2d1r-x2"):
+    for _dt in ("f32", "f64"):
+        WORKLOADS[f"{_n}-{_dt}-16384"] = (_n, "float32" if _dt == "f32" else "float64", 16384, 1000)
 DEFAULT = "star2d1r-f32-16384"
 
 
@@ -329,15 +333,26 @@ def run_an5d(args):
     if args.T:
         T = args.T
     dtype = getattr(torch, dtype_name)
-    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
-    ext = (n + 2 * rad,) * ndim
-    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    nf = 1
+    if name in inputs.SYSTEMS:   # multi-field system (NEXT N4): every field advanced by one kernel
+        ndim, rad, shape, nf, tab = inputs.system_problem(name)
+        div = 1.0
+        ext = (n + 2 * rad,) * ndim
+        st = an5d.System(ndim, rad, shape, tab, dtype)
+        a = an5d.empty_fields(nf, ext, rad, dtype, dev)
+        b = an5d.empty_fields(nf, ext, rad, dtype, dev)
+        for f in range(nf):
+            fill_uniform(a[f], inputs.DEFAULT_SEED + 0x1000 * f, ext)
+    else:
+        ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+        ext = (n + 2 * rad,) * ndim
+        st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+        a = an5d.empty_grid(ext, rad, dtype, dev)
+        b = an5d.empty_grid(ext, rad, dtype, dev)
+        fill_uniform(a, inputs.DEFAULT_SEED, ext)
     hint = {"bT": args.bt, "vec": args.vec, "h": args.h, "direct": args.direct, "n_thr": args.nthr}
     if getattr(args, "bsy", 0):
         hint["bS"] = [args.bsy, 0]
-    a = an5d.empty_grid(ext, rad, dtype, dev)
-    b = an5d.empty_grid(ext, rad, dtype, dev)
-    fill_uniform(a, inputs.DEFAULT_SEED, ext)
     # planner: the model's top 5 (b_T, vec) candidates run once each, fastest kept;
     # untimed, before the warm-up
     if args.no_tune:
@@ -367,9 +382,9 @@ def run_an5d(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    cells = float(n) ** ndim
+    cells = float(n) ** ndim * nf   # systems: cells of every field
     gcells = cells * T / (ms * 1e-3) / 1e9
-    F = perf.flops_per_cell(ndim, rad, shape, div != 1.0)
+    F = perf.flops_per_cell(ndim, rad, shape, div != 1.0, nf)
     peaks = _peaks()
     elem = 4 if dtype == torch.float32 else 8
     clock_mhz = peaks.get("sm_max_mhz") or 1965.0
@@ -380,7 +395,7 @@ def run_an5d(args):
     h_eff = geom["n_tiles"][0] * n / max(1, geom["n_units"]) if ndim == 2 else geom["h"]
     roof = perf.roofline(ndim=ndim, rad=rad, shape=shape, has_div=div != 1.0, dtype_bytes=elem, bT=cfg["bT"],
                          tile_loaded=geom["bS_loaded"][:nb], tile_compute=geom["compute"][:nb], h=h_eff,
-                         hbm_gbs=peaks["hbm_gbs"], fp_peak=fp_peak)
+                         hbm_gbs=peaks["hbm_gbs"], fp_peak=fp_peak, nf=nf)
 
     # ---- dominant kernel: one full-degree N.5D sweep (one persistent launch), timed per launch
     # with CUDA events on the launching stream, same grid and configuration as the step.
@@ -435,7 +450,7 @@ def run_an5d(args):
     # D2H of step i-1 overlap the sweeps of step i; PCIe is full duplex) when the grids are small
     # enough to double-buffer; otherwise serial on one stream.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and nf == 1:
         stor = a.untyped_storage()
         nbytes = stor.nbytes()
         k_e2e = max(2, min(args.steps, 5))
@@ -487,7 +502,7 @@ def run_an5d(args):
         del bufs
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and nf == 1:
         fill_uniform(a, inputs.DEFAULT_SEED, ext)
         host_grid = a.cpu().numpy()
         cpu = cpu_oracle_rate(name, dtype_name, n, host_grid, budget_s=args.cpu_budget)
@@ -498,7 +513,7 @@ def run_an5d(args):
         "unit": "GCells/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32" if dtype == torch.float32 else "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "stencil": name, "grid": list(ext), "T": T, "bT": cfg["bT"],
+        "config": {"workload": args.workload, "stencil": name, "grid": list(ext), "n_fields": nf, "T": T, "bT": cfg["bT"],
                    "vec": cfg["vec"], "h": cfg["h"], "n_thr": cfg["n_thr"], "partial_sums": "off" if cfg.get("direct") else "on",
                    "planner": "model" if args.no_tune else "model top-5, measured pick (P:784-793)",
                    "bS": geom["bS"][:nb], "bS_loaded": geom["bS_loaded"][:nb],

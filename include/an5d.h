@@ -134,6 +134,23 @@ typedef struct {
 an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* coeffs,
                         size_t n_coeffs, double divisor, an5d_dtype dtype, an5d_plan** out);
 
+/* A multi-field SYSTEM (NEXT N4: "multi-output temporal blocking to optimize multi-statement
+ * stencils"): n_fields arrays advance together, one statement per array, and statement i
+ * reads the PREVIOUS step of every array through its own Table-2-shaped table:
+ *     A_i'(x) = sum_j sum_d coeffs[i][j][d] * A_j(x + d)
+ * One sweep streams all arrays and carries every statement through b_T steps (2D kernels).
+ *   coeffs: n_fields * n_fields dense (2r+1)^ndim tables, block (i, j) at (i n_fields + j)(2r+1)^ndim,
+ *     each rounded once to dtype; STAR blocks must be 0 off-axis.  No divisor.
+ *   n_fields 1..8 (kernels are instantiated for 1 and 2; others: AN5D_ERR_UNSUPPORTED at run);
+ *   ndim 2 (3D with n_fields > 1: AN5D_ERR_UNSUPPORTED).
+ *   With n_fields > 1 every call taking `pitches` (an5d_run, an5d_sweep, an5d_copy_ring,
+ *   an5d_tune, an5d_plan_config, an5d_describe) reads pitches[0] = the element distance from one
+ *   field's array to the next (grids are n_fields arrays of identical layout, field-major; a
+ *   multiple of 16 bytes) followed by the ndim-1 usual pitches (NULL: dense fields and rows).
+ *   Slab runs (an5d_run_slab, an5d_sweep_peer with peers) take single-field plans only.        */
+an5d_status an5d_create_system(int ndim, int radius, an5d_shape shape, int n_fields, const double* coeffs,
+                               size_t n_coeffs, an5d_dtype dtype, an5d_plan** out);
+
 /* Advance the grid by T time steps (host loop of sweeps).
  *   grid_in / grid_out: device arrays with identical extents/pitches (the paper's A[2]).
  *   On return grid_out holds step T (interior) and the input ring; grid_in's interior is used as

@@ -121,6 +121,8 @@ def _load():
         "an5d_model_paper_search": (I32, [I32, I32, I32, I32, I32, pi64, ctypes.POINTER(DeviceParams), I32,
                                           ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_int)]),
+        "an5d_create_system": (I32, [I32, I32, I32, I32, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, I32,
+                                     ctypes.POINTER(P)]),
         "an5d_last_launch_count": (I64, [P]),
         "an5d_destroy": (I32, [P]),
         "an5d_last_error": (ctypes.c_char_p, []),
@@ -156,7 +158,7 @@ def load():
 def loaded() -> bool:
     return _LazyLib._h is not None
 
-EXPORTED_SYMBOLS = ("an5d_create", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_run_slab", "an5d_stream_signal",
+EXPORTED_SYMBOLS = ("an5d_create", "an5d_create_system", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_run_slab", "an5d_stream_signal",
                     "an5d_stream_wait", "an5d_ipc_export", "an5d_ipc_open", "an5d_ipc_close", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
                     "an5d_describe", "an5d_schedule", "an5d_model_paper", "an5d_model_paper_search",
                     "an5d_last_launch_count", "an5d_destroy", "an5d_last_error", "an5d_version")
@@ -294,6 +296,10 @@ class Stencil:
                                 c.size, float(divisor), dt, ctypes.byref(h)))
         self._h = h
 
+    @staticmethod
+    def _geom(t: torch.Tensor):
+        return _geom_of(t)
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value and _lib is not None:
@@ -303,8 +309,8 @@ class Stencil:
     # -- run / sweep ---------------------------------------------------------------------------
     def run(self, grid_in: torch.Tensor, grid_out: torch.Tensor, T: int, cfg=None, stream=None):
         """Advance T steps; result in grid_out (grid_in's interior is clobbered for T >= 2)."""
-        ext, pit = _geom_of(grid_in)
-        if list(grid_out.shape) != ext or [grid_out.stride(i) for i in range(grid_out.dim() - 1)] != pit:
+        ext, pit = self._geom(grid_in)
+        if list(grid_out.shape) != list(grid_in.shape) or grid_out.stride() != grid_in.stride():
             raise ValueError("grid_in and grid_out must have identical shape and strides")
         if grid_in.dtype != self.dtype or grid_out.dtype != self.dtype:
             raise ValueError("grid dtype does not match the stencil dtype")
@@ -320,7 +326,7 @@ class Stencil:
         """One sweep of `degree` time steps (slab mode; see an5d.h an5d_sweep).  ``peers``: None or
         a dict {"lo"/"hi": (device pointer int, plane shift, planes)} for the fused halo exchange
         (an5d_sweep_peer)."""
-        ext, pit = _geom_of(src)
+        ext, pit = self._geom(src)
         g = ext[0] if global_outer_extent is None else global_outer_extent
         lo = self.rad if out_lo is None else out_lo
         hi = ext[0] - self.rad if out_hi is None else out_hi
@@ -349,7 +355,7 @@ class Stencil:
         """One slab's T-step run with the fused halo exchange (an5d_run_slab).  ``lo`` / ``hi``:
         None or (neighbour buffer paired with grid_in, with grid_out, plane shift, flag pointer).
         Returns the new epoch."""
-        ext, pit = _geom_of(grid_in)
+        ext, pit = self._geom(grid_in)
         st = stream if stream is not None else torch.cuda.current_stream(grid_in.device)
         L = SlabLinks()
         for k, side in enumerate((lo, hi)):
@@ -369,7 +375,7 @@ class Stencil:
 
     def copy_ring(self, src: torch.Tensor, dst: torch.Tensor, outer_offset: int = 0,
                   global_outer_extent: int | None = None, stream=None):
-        ext, pit = _geom_of(src)
+        ext, pit = self._geom(src)
         g = ext[0] if global_outer_extent is None else global_outer_extent
         st = stream if stream is not None else torch.cuda.current_stream(src.device)
         _check(_lib.an5d_copy_ring(self._h, src.data_ptr(), dst.data_ptr(), _i64(ext), _i64(pit),
@@ -388,7 +394,7 @@ class Stencil:
         """Model top-k + measured pick (an5d_tune).  Reads grid_in, overwrites grid_out's
         interior; blocks until the candidate sweeps are timed.  Returns the config with the measured
         "seconds_per_cell_step" of the winner."""
-        ext, pit = _geom_of(grid_in)
+        ext, pit = self._geom(grid_in)
         st = stream if stream is not None else torch.cuda.current_stream(grid_in.device)
         out = Config()
         best = ctypes.c_double()
@@ -443,3 +449,61 @@ def ipc_close(base: int):
 
 def version() -> str:
     return _lib.an5d_version().decode()
+
+
+def empty_fields(n_fields: int, extents, rad: int, dtype=torch.float32, device="cuda"):
+    """n_fields grids of identical layout (see empty_grid), field-major in one allocation: a view of
+    shape (n_fields, *extents) whose field stride is a multiple of 128 bytes (an5d_create_system)."""
+    extents = [int(e) for e in extents]
+    elem = torch.empty((), dtype=dtype).element_size()
+    A = 16 // elem
+    pitch = -(-extents[-1] // (128 // elem)) * (128 // elem)
+    strides = [1]
+    if len(extents) >= 2:
+        strides.insert(0, pitch)
+    if len(extents) == 3:
+        strides.insert(0, pitch * extents[1])
+    fstride = -(-(strides[0] * extents[0]) // (128 // elem)) * (128 // elem)
+    buf = torch.empty(fstride * n_fields + 2 * A, dtype=dtype, device=device)
+    off = (A - rad % A) % A
+    return torch.as_strided(buf, [n_fields] + extents, [fstride] + strides, storage_offset=off)
+
+
+def to_fields(t: torch.Tensor, rad: int):
+    """Copy a (n_fields, *grid) tensor into an aligned field-major view (see empty_fields)."""
+    g = empty_fields(t.shape[0], t.shape[1:], rad, t.dtype, t.device)
+    g.copy_(t)
+    return g
+
+
+class System(Stencil):
+    """A multi-field system (an5d_create_system; NEXT N4): n_fields arrays advance together,
+    statement i reading the previous step of every array through block [i, j] of ``coeffs``
+    (shape (n_fields, n_fields, (2r+1,)*ndim)).  Grids are (n_fields, *extents) tensors from
+    empty_fields / to_fields; run / sweep / tune / copy_ring / describe as for Stencil."""
+
+    def __init__(self, ndim: int, rad: int, shape: int, coeffs, dtype=torch.float32):
+        import numpy as np
+
+        c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64))
+        nf = c.shape[0]
+        if c.shape[:2] != (nf, nf):
+            raise ValueError("coeffs must have shape (n_fields, n_fields, table)")
+        c = c.reshape(-1)
+        self.ndim, self.rad, self.shape, self.divisor, self.n_fields = ndim, rad, shape, 1.0, nf
+        self.dtype = dtype
+        self.coeffs = c
+        dt = F32 if dtype == torch.float32 else F64
+        h = ctypes.c_void_p()
+        _check(_lib.an5d_create_system(ndim, rad, shape, nf, c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       c.size, dt, ctypes.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def _geom(t: torch.Tensor):
+        """(n_fields, *grid) tensor -> extents of one grid, pitches = [field stride, grid pitches]."""
+        if not t.is_cuda:
+            raise ValueError("grids must be CUDA tensors (no CPU path)")
+        if t.dtype not in (torch.float32, torch.float64) or t.dim() not in (3, 4) or t.stride(-1) != 1:
+            raise ValueError("fields must be a (n_fields, *grid) float32/float64 tensor with unit x stride")
+        return list(t.shape[1:]), [t.stride(i) for i in range(t.dim() - 1)]

@@ -59,6 +59,8 @@ CORE = {
 }
 # partial sums OFF (direct gather, BASELINE config 4 = box2d2r fp32): vec 8 and 4, b_T 1..2
 CORE_DIRECT = {(2, 0, 1, 2): [(8, 2), (4, 2)]}
+# multi-field systems (NEXT N4): 2 fields advanced together, layout "x2" (NF = 2)
+CORE_SYSTEM = {(2, 0, 0, 1): [(8, 4), (4, 5)], (2, 0, 1, 1): [(8, 3)], (2, 1, 0, 1): [(4, 3)], (2, 1, 1, 1): [(4, 2)]}
 # gradient2d (shape 2, Table 2, NEXT N3): non-linear, direct gather only
 CORE_GRAD = {(2, 0, 2, 1): [(8, 4), (4, 4)], (2, 1, 2, 1): [(4, 3)]}
 # 3D 512-thread layouts (kernel3d.cuh Kernel3DTraits): "t32x2" = 32 x 16 threads with 2-cell patch
@@ -134,6 +136,9 @@ def core_instances():
     for (ndim, dtype, shape, rad), lst in CORE_LAYOUTS.items():
         for vec, bmax, lay in lst:
             out += [(ndim, dtype, shape, rad, bT, vec, 1, lay) for bT in range(1, bmax + 1)]
+    for (ndim, dtype, shape, rad), lst in CORE_SYSTEM.items():
+        for vec, bmax in lst:
+            out += [(ndim, dtype, shape, rad, bT, vec, 1, "x2") for bT in range(1, bmax + 1)]
     for (ndim, dtype, shape, rad), lst in CORE_SPLIT.items():
         for vec, bmax in lst:
             out += [(ndim, dtype, shape, rad, bT, vec, 1, "w2") for bT in range(2, bmax + 1)]
@@ -187,6 +192,8 @@ def generate():
             targs += ", 1, true"   # gradient2d (GRAD template flag)
         if layout == "w2":
             targs += ", true, 2"
+        elif layout == "x2":
+            targs += ", true, 1, false, 2"   # NF = 2 fields
         elif layout:
             targs += ", %d, %d, %d" % LAYOUTS[layout]
         fn = "make_instance2d" if ndim == 2 else "make_instance3d"

@@ -57,6 +57,7 @@ an5d_status set_error(an5d_status s, const char* msg) {
 // ---------------------------------------------------------------------------------------------
 struct Plan {
     int ndim, rad, shape, dtype;
+    int nf = 1;                        // fields advanced together (an5d_create_system; NEXT N4)
     size_t elem;                       // bytes per cell (n_word)
     std::vector<double> coeffs_folded; // dense table / divisor (P:596-602 reciprocal folding)
     std::vector<unsigned char> coeffs_dev_t;  // rounded to dtype, as raw bytes
@@ -113,7 +114,7 @@ const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0, in
     for (const Instance& i : registry())
         if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad && i.bT == bT &&
             i.vec == vec && i.assoc == (direct ? 0 : 1) && (!tile_x || i.tile_x_loaded == tile_x) &&
-            (!n_thr || i.threads == n_thr) && (!tile_y || i.tile_y == tile_y))
+            (!n_thr || i.threads == n_thr) && (!tile_y || i.tile_y == tile_y) && std::max(1, i.nf) == p.nf)
             if (!best || std::make_tuple(i.tile_x_loaded, i.threads, i.tile_y) <
                              std::make_tuple(best->tile_x_loaded, best->threads, best->tile_y))
                 best = &i;
@@ -133,7 +134,7 @@ int cfg_tile_x(const Plan& p, const an5d_config& c) {
 // halo is not rounded, so the loaded height is b_S_y itself; it names the cluster layouts (a
 // cluster of CL blocks is one tile of CL x 16 VY rows, NEXT N2).
 int cfg_tile_y(const Plan& p, const an5d_config& c) {
-    return (p.ndim == 3 && c.bT) ? c.bS[0] : 0;
+    return p.ndim == 3 ? c.bS[0] : 0;
 }
 
 // The instance a sweep of degree d runs under configuration c: the configuration's layout, or for
@@ -158,6 +159,7 @@ int max_bT_for(const Plan& p, int vec) {
 struct Dims {
     int64_t E[3];      // extents outer..x (ndim entries used)
     int64_t pitch[2];  // outer strides (2D: pitch[0] = row; 3D: pitch[0] = plane, pitch[1] = row)
+    int64_t fstride = 0;  // multi-field systems: elements from one field's array to the next
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -434,9 +436,9 @@ double model_time(const Plan& p, const Instance& inst, const Dims& dm, int bT, i
         units = (double)build_runs(p.ndim, g, W, run_frac()).size();
         unit_rows = nt * (double)(dm.E[0] - 2 * R) / units + 2.0 * bT * R;
     }
-    const double bytes = (double)p.elem * (units * unit_rows * cells_per_plane + (double)interior);
+    const double bytes = (double)p.elem * p.nf * (units * unit_rows * cells_per_plane + (double)interior);
     const double t_hbm = bytes / (di.hbm_gbs * 1e9 * eta_hbm);
-    const double fma_ops = units * (unit_rows + 2 * R + 1) * cells_per_plane * bT * taps_of(p);
+    const double fma_ops = units * (unit_rows + 2 * R + 1) * cells_per_plane * bT * taps_of(p) * p.nf * p.nf;
     const double lanes = p.dtype == AN5D_F64 ? 64.0 : 128.0;
     const double t_fma = fma_ops / (di.n_sm * lanes * di.clock_ghz * 1e9 * eta_fma);
     const double tail = 1.0 + resident / std::max<double>(1.0, (double)g.n_units);
@@ -561,6 +563,9 @@ an5d_status launch_copy(Plan& p, const void* src, void* dst, const Dims& dm, boo
     const int64_t py = is3d ? dm.pitch[1] : dm.pitch[0];
     const unsigned grid = (unsigned)std::min<int64_t>(nrows, 148 * 32);
     const int thr = ring_only ? 128 : 256;
+    for (int f = 0; f < p.nf; ++f) {   // every field of a system (one for a plain stencil)
+    src = static_cast<const char*>(src) + (f ? dm.fstride * (int64_t)p.elem : 0);
+    dst = static_cast<char*>(dst) + (f ? dm.fstride * (int64_t)p.elem : 0);
     if (p.dtype == AN5D_F32) {
         if (ring_only)
             ring_copy_kernel<float><<<grid, thr, 0, st>>>((const float*)src, (float*)dst, nrows, Ey, Ex, pz, py,
@@ -576,6 +581,7 @@ an5d_status launch_copy(Plan& p, const void* src, void* dst, const Dims& dm, boo
                                                       is3d);
     }
     p.launches++;
+    }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? AN5D_OK : cuda_fail(e, "copy kernel launch");
 }
@@ -671,6 +677,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.h = g.h; a.n_units = g.n_units; a.n_sb = g.n_sb;
         a.ctr = p.ctr + 2 * (p.ctr_seq++ % kCtrRing);
         a.wc = wc; a.Ex = (int)dm.E[1]; a.C = g.C[0]; a.H = g.halo[0]; a.n_tiles_x = (int)g.ntiles[0];
+        a.fstride = dm.fstride;
         set_peers(a, peers, dm.pitch[0], out_lo, out_hi);
         const int64_t cap = (int64_t)resident_blocks(*inst) * dev_info().n_sm;
         const int64_t blocks = std::min<int64_t>(g.n_units, cap);
@@ -766,6 +773,10 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
 
 an5d_status read_dims(const Plan& p, const int64_t* extents, const int64_t* pitches, Dims& dm) {
     if (!extents) return fail(AN5D_ERR_INVALID_ARGUMENT, "extents is NULL");
+    if (p.nf > 1 && pitches) {   // systems: pitches = {field stride, the usual ndim-1 pitches}
+        dm.fstride = pitches[0];
+        pitches += 1;
+    }
     for (int i = 0; i < p.ndim; ++i) {
         dm.E[i] = extents[i];
         if (dm.E[i] < 2 * p.rad + 1)
@@ -777,6 +788,9 @@ an5d_status read_dims(const Plan& p, const int64_t* extents, const int64_t* pitc
     if (p.ndim == 2) {
         dm.pitch[0] = pitches ? pitches[0] : dm.E[1];
         if (dm.pitch[0] < dm.E[1]) return fail(AN5D_ERR_SHAPE_MISMATCH, "row pitch < x extent");
+        if (p.nf > 1 && !dm.fstride) dm.fstride = dm.E[0] * dm.pitch[0];   // NULL pitches: dense fields
+        if (p.nf > 1 && dm.fstride < dm.E[0] * dm.pitch[0])
+            return fail(AN5D_ERR_SHAPE_MISMATCH, "field stride < rows * pitch (fields overlap)");
     } else {
         dm.pitch[1] = pitches ? pitches[1] : dm.E[2];
         dm.pitch[0] = pitches ? pitches[0] : dm.E[1] * dm.pitch[1];
@@ -793,6 +807,8 @@ an5d_status check_alignment(const Plan& p, const void* ptr, const Dims& dm, cons
     for (int i = 0; i < p.ndim - 1; ++i)
         if ((dm.pitch[i] * (int64_t)p.elem) % 16)
             return fail(AN5D_ERR_UNSUPPORTED, "%s: pitch[%d]*elem_size not a multiple of 16 bytes", name, i);
+    if ((dm.fstride * (int64_t)p.elem) % 16)
+        return fail(AN5D_ERR_UNSUPPORTED, "%s: field stride*elem_size not a multiple of 16 bytes", name);
     return AN5D_OK;
 }
 
@@ -978,6 +994,52 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
             const std::vector<double> f = fold_coefficients<double>(coeffs, n, divisor);
             memcpy(p->coeffs_dev_t.data(), f.data(), n * 8);
             for (size_t k = 0; k < n; ++k) p->coeffs_folded[k] = f[k];
+        }
+        *out = p;
+        return AN5D_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(AN5D_ERR_OUT_OF_MEMORY, "host allocation failed");
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
+an5d_status an5d_create_system(int ndim, int radius, an5d_shape shape, int n_fields, const double* coeffs,
+                               size_t n_coeffs, an5d_dtype dtype, an5d_plan** out) {
+    try {
+        if (!out) return fail(AN5D_ERR_INVALID_ARGUMENT, "out is NULL");
+        *out = nullptr;
+        if (n_fields < 1 || n_fields > 8) return fail(AN5D_ERR_INVALID_ARGUMENT, "n_fields must be 1..8");
+        if (shape != AN5D_STAR && shape != AN5D_BOX) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad shape");
+        if (ndim != 2 && ndim != 3) return fail(AN5D_ERR_INVALID_ARGUMENT, "ndim must be 2 or 3");
+        if (radius < 1 || radius > 4) return fail(AN5D_ERR_INVALID_ARGUMENT, "radius must be 1..4");
+        if (dtype != AN5D_F32 && dtype != AN5D_F64) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad dtype");
+        if (!coeffs) return fail(AN5D_ERR_INVALID_ARGUMENT, "coeffs is NULL");
+        const int w = 2 * radius + 1;
+        const size_t n = ndim == 2 ? (size_t)w * w : (size_t)w * w * w;
+        const size_t nb = (size_t)n_fields * n_fields;
+        if (n_coeffs != n * nb)
+            return fail(AN5D_ERR_SHAPE_MISMATCH, "expected %zu coefficients (n_fields^2 (2r+1)^ndim), got %zu", n * nb,
+                        n_coeffs);
+        if (ndim != 2 && n_fields > 1) return fail(AN5D_ERR_UNSUPPORTED, "multi-field systems are 2D");
+        an5d_plan* p = nullptr;
+        an5d_status s = an5d_create(ndim, radius, shape, coeffs, n, 1.0, dtype, &p);   // validates block 0
+        if (s != AN5D_OK) return s;
+        p->nf = n_fields;
+        p->coeffs_dev_t.resize(n * nb * p->elem);
+        for (size_t k = 0; k < n * nb; ++k) {
+            int rem = (int)(k % n), nz = 0;
+            for (int i = 0; i < ndim; ++i) { nz += (rem % w) != radius; rem /= w; }
+            if (!std::isfinite(coeffs[k]) || (shape == AN5D_STAR && nz > 1 && coeffs[k] != 0.0)) {
+                an5d_destroy(p);
+                return fail(AN5D_ERR_SHAPE_MISMATCH, "bad coefficient %zu (non-finite or STAR off-axis)", k);
+            }
+            if (dtype == AN5D_F32) {   // rounded once to the dtype (nothing to fold: no divisor)
+                const float f = (float)coeffs[k];
+                memcpy(p->coeffs_dev_t.data() + k * 4, &f, 4);
+            } else {
+                memcpy(p->coeffs_dev_t.data() + k * 8, &coeffs[k], 8);
+            }
         }
         *out = p;
         return AN5D_OK;
@@ -1270,6 +1332,7 @@ an5d_status an5d_sweep_peer(an5d_plan* p, const void* src, void* dst, const int6
                             void* stream) {
     try {
         if (!p || !cfg) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (p->nf > 1 && peers) return fail(AN5D_ERR_UNSUPPORTED, "peer stores: single-field plans only");
         Dims dm{};
         an5d_status s = read_dims(*p, extents, pitches, dm);
         if (s != AN5D_OK) return s;
@@ -1411,6 +1474,7 @@ an5d_status an5d_run_slab(an5d_plan* p, void* grid_in, void* grid_out, const int
                           int64_t own_lo, int64_t own_hi, an5d_slab_links* links, void* stream) {
     try {
         if (!p || !links || !links->flag) return fail(AN5D_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (p->nf > 1) return fail(AN5D_ERR_UNSUPPORTED, "slab runs: single-field plans only");
         if (T < 0) return fail(AN5D_ERR_INVALID_ARGUMENT, "T < 0");
         Dims dm{};
         an5d_status s = read_dims(*p, extents, pitches, dm);

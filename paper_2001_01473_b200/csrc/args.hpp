@@ -30,6 +30,7 @@ struct Sweep2DArgs {
     void* peer_hi;
     int64_t peer_lo_shift, peer_hi_shift;
     int64_t send_lo_end, send_hi_begin;
+    int64_t fstride;      // multi-field systems: element distance between consecutive fields (0: one field)
     int Ex;               // x extent (ring included)
     int C;                // compute width per tile (aligned to 16 bytes)
     int H;                // loaded halo per side (>= degree*rad, multiple of the vector width)

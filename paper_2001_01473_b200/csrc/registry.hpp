@@ -29,6 +29,7 @@ struct Instance {
     int tile_y;                              // 3D: cells per tile along y; 2D: 0
     size_t smem_bytes;                       // dynamic shared memory per block
     int cluster;                             // 3D: blocks per cluster along y (tile_y = cluster x block rows)
+    int nf;                                  // fields advanced together (multi-field systems; 0/1 = one)
 };
 
 std::vector<Instance>& registry();

@@ -16,27 +16,28 @@ def n_taps(ndim: int, rad: int, shape: int) -> int:
     return (2 * rad + 1) ** ndim if shape == BOX else 2 * ndim * rad + 1
 
 
-def flops_per_cell(ndim: int, rad: int, shape: int, has_div: bool) -> int:
+def flops_per_cell(ndim: int, rad: int, shape: int, has_div: bool, nf: int = 1) -> int:
     """Table 2: k products summed = k FMA-equivalent ops counted as 2k-1 FLOPs, +1 for /c_0;
-    gradient2d: the printed 19."""
+    gradient2d: the printed 19.  Multi-field systems (nf > 1): per cell of one field,
+    its statement sums nf x taps products (2 nf taps - 1 FLOPs)."""
     if shape == GRAD:
         return 19
-    return 2 * n_taps(ndim, rad, shape) - 1 + (1 if has_div else 0)
+    return 2 * nf * n_taps(ndim, rad, shape) - 1 + (1 if has_div else 0)
 
 
-def op_mix(ndim: int, rad: int, shape: int, has_div: bool):
+def op_mix(ndim: int, rad: int, shape: int, has_div: bool, nf: int = 1):
     """(n_FMA, n_MUL, n_ADD + n_OTHER) per cell under the paper's mapping.
     gradient2d: 2 FMA (a square added to a square), 3 MUL (two squares, c f),
     4 differences + 3 adds, and sqrt + division counted as OTHER (R-17)."""
     if shape == GRAD:
         return 2, 3, 9
-    k = n_taps(ndim, rad, shape)
+    k = nf * n_taps(ndim, rad, shape)
     return k - 1, 1 + (1 if has_div else 0), 0
 
 
-def eff_alu(ndim: int, rad: int, shape: int, has_div: bool) -> float:
+def eff_alu(ndim: int, rad: int, shape: int, has_div: bool, nf: int = 1) -> float:
     """eff_ALU = (2 FMA + MUL + ADD + OTHER) / (2 (FMA + MUL + ADD + OTHER))."""
-    f, m, a = op_mix(ndim, rad, shape, has_div)
+    f, m, a = op_mix(ndim, rad, shape, has_div, nf)
     return (2 * f + m + a) / (2 * (f + m + a))
 
 
@@ -48,7 +49,7 @@ def fp_peak_flops(dtype_bytes: int, n_sm: int = 148, clock_mhz: float = 1965.0) 
 
 
 def roofline(*, ndim, rad, shape, has_div, dtype_bytes, bT, tile_loaded, tile_compute, h, hbm_gbs,
-             fp_peak):
+             fp_peak, nf=1):
     """b_T-adjusted roofline in cells/s for a configuration.
 
     With the logical tile b_i = C_i + 2 b_T rad (the paper's b_S incl. halo), compute
@@ -64,8 +65,8 @@ def roofline(*, ndim, rad, shape, has_div, dtype_bytes, bT, tile_loaded, tile_co
     reported separately as R_read_kernel / R_comp_kernel.
     """
     import math
-    F = flops_per_cell(ndim, rad, shape, has_div)
-    eff = eff_alu(ndim, rad, shape, has_div)
+    F = flops_per_cell(ndim, rad, shape, has_div, nf)      # per cell of one field (nf: systems)
+    eff = eff_alu(ndim, rad, shape, has_div, nf)
     C = list(tile_compute)
     b = [c + 2 * bT * rad for c in C]
     pc = math.prod(C)
