@@ -58,7 +58,8 @@ typedef enum {
     AN5D_ERR_UNSUPPORTED = 5,        /* no kernel instance for (ndim,rad,shape,dtype,b_T,vec),   */
                                      /* or misaligned base/pitch for the vector path            */
     AN5D_ERR_CUDA = 6,               /* a CUDA runtime error (message in an5d_last_error)       */
-    AN5D_ERR_OUT_OF_MEMORY = 7
+    AN5D_ERR_OUT_OF_MEMORY = 7,
+    AN5D_ERR_NCCL = 8                /* NCCL missing or failed (an5d_set_comm slab mode)         */
 } an5d_status;
 
 /* STAR / BOX: P:127-142.  GRADIENT: the non-linear gradient2d row of Table 2, 2D,
@@ -234,6 +235,31 @@ an5d_status an5d_run_slab(an5d_plan* plan, void* grid_in, void* grid_out, const 
                           const int64_t* pitches, int64_t T, const an5d_config* cfg, int64_t outer_offset,
                           int64_t global_outer_extent, int64_t own_lo, int64_t own_hi,
                           an5d_slab_links* links, void* cuda_stream);
+
+/* ---- Library-owned NCCL slab mode (BASELINE north_star (d):
+ * "slab decomposition of the outermost dimension ... exchanging bT*rad-deep halos every bT steps
+ * (NCCL send/recv), overlapped with interior compute") ------------------------------------------
+ * an5d_comm_unique_id: ncclGetUniqueId into out128 (128 bytes).  Rank 0 calls it and hands the
+ *   bytes to the other ranks out of band (e.g. torch.distributed.broadcast_object_list).
+ * an5d_set_comm: the plan joins an NCCL communicator of nranks ranks (ncclCommInitRank; one
+ *   process per GPU, the current device; collective: every rank calls it).  From then on an5d_run
+ *   treats its grids as this rank's slab of the streaming (outermost) dimension: local plane 0 is
+ *   global plane outer_offset of a global array of global_outer_extent planes; on each side that
+ *   has a neighbour (rank > 0 below, rank < nranks-1 above) the outermost ghost_planes local
+ *   planes are the neighbour's (ghost_planes >= b_T*rad of the run, else AN5D_ERR_UNSUPPORTED
+ *   before any launch).  grid_in must hold the input on every local plane, ghosts included; on
+ *   return (stream-ordered) grid_out's owned planes hold step T.  Per sweep of degree d: the
+ *   boundary output planes first, then the d_next*rad outermost owned planes of the output are
+ *   ncclSend/ncclRecv-exchanged with the neighbours in one group on a library-owned comm stream
+ *   while the interior planes are computed on cuda_stream; the next sweep waits for both.
+ *   Every rank must run the same T and configuration.  nranks == 1: a plain run.
+ *   nccl_unique_id == NULL: detach (destroys the communicator).  NCCL is loaded at run time
+ *   ("libnccl.so.2" -- the one the process already has, e.g. torch's; AN5D_NCCL_LIB overrides);
+ *   a missing library or an NCCL failure -> AN5D_ERR_NCCL.  Single-field plans only.
+ *   The fused exchange (an5d_run_slab) is the alternative without NCCL on the data path.       */
+an5d_status an5d_comm_unique_id(void* out128);
+an5d_status an5d_set_comm(an5d_plan* plan, const void* nccl_unique_id, int rank, int nranks,
+                          int64_t global_outer_extent, int64_t outer_offset, int ghost_planes);
 
 /* Copy the rad-wide ring cells of src into dst (O(surface) kernel).  With outer_offset /
  * global_outer_extent as in an5d_sweep, only global ring planes/rows/columns are copied.       */

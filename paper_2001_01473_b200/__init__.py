@@ -23,7 +23,7 @@ F32, F64 = 0, 1
 STATUS = {
     0: "AN5D_OK", 1: "AN5D_ERR_INVALID_ARGUMENT", 2: "AN5D_ERR_INFEASIBLE_CONFIG",
     3: "AN5D_ERR_BLOCK_TOO_LARGE", 4: "AN5D_ERR_SHAPE_MISMATCH", 5: "AN5D_ERR_UNSUPPORTED",
-    6: "AN5D_ERR_CUDA", 7: "AN5D_ERR_OUT_OF_MEMORY",
+    6: "AN5D_ERR_CUDA", 7: "AN5D_ERR_OUT_OF_MEMORY", 8: "AN5D_ERR_NCCL",
 }
 
 
@@ -123,6 +123,8 @@ def _load():
                                           ctypes.POINTER(ctypes.c_int)]),
         "an5d_create_system": (I32, [I32, I32, I32, I32, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, I32,
                                      ctypes.POINTER(P)]),
+        "an5d_comm_unique_id": (I32, [P]),
+        "an5d_set_comm": (I32, [P, P, I32, I32, I64, I64, I32]),
         "an5d_last_launch_count": (I64, [P]),
         "an5d_destroy": (I32, [P]),
         "an5d_last_error": (ctypes.c_char_p, []),
@@ -158,7 +160,7 @@ def load():
 def loaded() -> bool:
     return _LazyLib._h is not None
 
-EXPORTED_SYMBOLS = ("an5d_create", "an5d_create_system", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_run_slab", "an5d_stream_signal",
+EXPORTED_SYMBOLS = ("an5d_create", "an5d_create_system", "an5d_comm_unique_id", "an5d_set_comm", "an5d_run", "an5d_sweep", "an5d_sweep_peer", "an5d_run_slab", "an5d_stream_signal",
                     "an5d_stream_wait", "an5d_ipc_export", "an5d_ipc_open", "an5d_ipc_close", "an5d_copy_ring", "an5d_plan_config", "an5d_tune",
                     "an5d_describe", "an5d_schedule", "an5d_model_paper", "an5d_model_paper_search",
                     "an5d_last_launch_count", "an5d_destroy", "an5d_last_error", "an5d_version")
@@ -373,6 +375,14 @@ class Stencil:
                                   int(own_hi), ctypes.byref(L), ctypes.c_void_p(st.cuda_stream)))
         return int(L.epoch)
 
+    def set_comm(self, unique_id: bytes | None, rank: int = 0, nranks: int = 1, global_outer_extent: int = 0,
+                 outer_offset: int = 0, ghost_planes: int = 0):
+        """Join an NCCL communicator (an5d_set_comm): later runs treat the grids as this rank's slab
+        and exchange ghost planes with ncclSend/ncclRecv inside the library.  None detaches."""
+        uid = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+        _check(_lib.an5d_set_comm(self._h, uid, int(rank), int(nranks), int(global_outer_extent), int(outer_offset),
+                                  int(ghost_planes)))
+
     def copy_ring(self, src: torch.Tensor, dst: torch.Tensor, outer_offset: int = 0,
                   global_outer_extent: int | None = None, stream=None):
         ext, pit = self._geom(src)
@@ -445,6 +455,13 @@ def ipc_open(handle: bytes) -> int:
 
 def ipc_close(base: int):
     _check(_lib.an5d_ipc_close(ctypes.c_void_p(int(base))))
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id for an5d_set_comm (call on rank 0, broadcast to the others)."""
+    b = ctypes.create_string_buffer(128)
+    _check(_lib.an5d_comm_unique_id(b))
+    return b.raw
 
 
 def version() -> str:

@@ -2,6 +2,8 @@
 // B200 planner, launch orchestration.  Product code: shares nothing with oracle/.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no libcuda link)
+#include <dlfcn.h>
+#include <nccl.h>           // types only: NCCL is loaded at run time (an5d_set_comm)
 
 #include <algorithm>
 #include <cmath>
@@ -58,6 +60,12 @@ an5d_status set_error(an5d_status s, const char* msg) {
 struct Plan {
     int ndim, rad, shape, dtype;
     int nf = 1;                        // fields advanced together (an5d_create_system; NEXT N4)
+    // NCCL slab mode (an5d_set_comm): this rank's slab of the streaming dimension
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1, ghost = 0;
+    int64_t gE0 = 0, outer_offset = 0;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_xchg = nullptr;
     size_t elem;                       // bytes per cell (n_word)
     std::vector<double> coeffs_folded; // dense table / divisor (P:596-602 reciprocal folding)
     std::vector<unsigned char> coeffs_dev_t;  // rounded to dtype, as raw bytes
@@ -931,6 +939,139 @@ F driver_fn(const char* name) {
 }  // namespace
 
 // =============================================================================================
+// NCCL slab mode (an5d_set_comm).  NCCL is loaded at run time so the
+// library never pins a second NCCL next to the one the process (torch) already has.
+// =============================================================================================
+namespace {
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = nullptr;
+    if (const char* e = getenv("AN5D_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);   // already in the process
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { api.why = std::string("cannot load libnccl.so.2: ") + dlerror(); return api; }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+             api.GroupEnd && api.GetErrorString;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+    return api;
+}
+
+an5d_status nccl_fail(ncclResult_t r, const char* what) {
+    return fail(AN5D_ERR_NCCL, "%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "NCCL error");
+}
+
+// One rank's T-step run of its slab with the NCCL exchange (mirrors slab.py run_distributed):
+// per sweep the boundary output planes first, then the d_next rad outermost owned planes are
+// sent to / received from the neighbours on the plan's comm stream while the interior planes are
+// computed on `st`; the next sweep waits for the exchange.
+an5d_status run_comm(Plan& p, void* grid_in, void* grid_out, const Dims& dm, int64_t T, const an5d_config& c,
+                     cudaStream_t st) {
+    const NcclApi& api = nccl();
+    std::vector<int> deg;
+    bool tc = false;
+    make_schedule(T, c.bT, deg, tc);
+    const int R = p.rad;
+    const bool lower = p.rank > 0, upper = p.rank < p.nranks - 1;
+    const int64_t E0 = dm.E[0];
+    const int64_t out_lo = lower ? p.ghost : std::max<int64_t>(0, R - p.outer_offset);
+    const int64_t out_hi = upper ? E0 - p.ghost : std::min<int64_t>(E0, p.gE0 - R - p.outer_offset);
+    if ((lower || upper) && p.ghost < c.bT * R)
+        return fail(AN5D_ERR_UNSUPPORTED, "ghost_planes %d < b_T * rad = %d", p.ghost, c.bT * R);
+    if (out_hi <= out_lo) return fail(AN5D_ERR_SHAPE_MISMATCH, "slab owns no plane");
+    for (int d : deg) {   // validate every sweep before the first launch
+        const Instance* inst = find_instance(p, d, c);
+        SweepGeom g{};
+        an5d_status s = sweep_geometry(p, *inst, dm, d, c.h, p.outer_offset, p.gE0, out_lo, out_hi, g);
+        if (s != AN5D_OK) return s;
+    }
+    an5d_status s = launch_copy(p, grid_in, grid_out, dm, true, p.outer_offset, p.gE0, st);
+    if (s != AN5D_OK) return s;
+    const size_t plane_bytes = (size_t)dm.pitch[0] * p.elem;
+    void* bufs[2] = {grid_in, grid_out};
+    bool pending = false;
+    cudaError_t e;
+    for (size_t i = 0; i < deg.size(); ++i) {
+        const void* src = bufs[i % 2];
+        char* dst = static_cast<char*>(bufs[(i + 1) % 2]);
+        const int d = deg[i], nd = i + 1 < deg.size() ? deg[i + 1] : 0;
+        const int64_t g = (int64_t)nd * R, hb = std::max<int64_t>(g, c.h);
+        int64_t blo = (lower && g) ? out_lo + hb : out_lo, bhi = (upper && g) ? out_hi - hb : out_hi;
+        std::vector<std::pair<int64_t, int64_t>> boundary, interior;
+        if (blo >= bhi) {
+            boundary.emplace_back(out_lo, out_hi);
+        } else {
+            if (blo > out_lo) boundary.emplace_back(out_lo, blo);
+            if (out_hi > bhi) boundary.emplace_back(bhi, out_hi);
+            interior.emplace_back(blo, bhi);
+        }
+        if (pending && (e = cudaStreamWaitEvent(st, p.ev_xchg, 0)) != cudaSuccess) return cuda_fail(e, "wait exchange");
+        pending = false;
+        for (auto& r : boundary)
+            if ((s = launch_sweep(p, src, dst, dm, d, c, p.outer_offset, p.gE0, r.first, r.second, nullptr, nullptr,
+                                  false, st)) != AN5D_OK)
+                return s;
+        if (g && (lower || upper)) {
+            if ((e = cudaEventRecord(p.ev_bnd, st)) != cudaSuccess) return cuda_fail(e, "event");
+            if ((e = cudaStreamWaitEvent(p.comm_stream, p.ev_bnd, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+            ncclResult_t r = api.GroupStart();
+            if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+            const size_t n = (size_t)g * plane_bytes;
+            if (lower) {
+                if ((r = api.Send(dst + out_lo * plane_bytes, n, ncclUint8, p.rank - 1, p.comm, p.comm_stream)) != ncclSuccess)
+                    return nccl_fail(r, "ncclSend");
+                if ((r = api.Recv(dst + (out_lo - g) * plane_bytes, n, ncclUint8, p.rank - 1, p.comm, p.comm_stream)) !=
+                    ncclSuccess)
+                    return nccl_fail(r, "ncclRecv");
+            }
+            if (upper) {
+                if ((r = api.Send(dst + (out_hi - g) * plane_bytes, n, ncclUint8, p.rank + 1, p.comm, p.comm_stream)) !=
+                    ncclSuccess)
+                    return nccl_fail(r, "ncclSend");
+                if ((r = api.Recv(dst + out_hi * plane_bytes, n, ncclUint8, p.rank + 1, p.comm, p.comm_stream)) != ncclSuccess)
+                    return nccl_fail(r, "ncclRecv");
+            }
+            if ((r = api.GroupEnd()) != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+            if ((e = cudaEventRecord(p.ev_xchg, p.comm_stream)) != cudaSuccess) return cuda_fail(e, "event");
+            pending = true;
+        }
+        for (auto& r : interior)
+            if ((s = launch_sweep(p, src, dst, dm, d, c, p.outer_offset, p.gE0, r.first, r.second, nullptr, nullptr,
+                                  false, st)) != AN5D_OK)
+                return s;
+    }
+    if (pending && (e = cudaStreamWaitEvent(st, p.ev_xchg, 0)) != cudaSuccess) return cuda_fail(e, "wait exchange");
+    if (tc) return launch_copy(p, grid_in, grid_out, dm, false, 0, E0, st);   // b_T = 1, even count
+    return AN5D_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
 // C ABI
 // =============================================================================================
 extern "C" {
@@ -1050,8 +1191,61 @@ an5d_status an5d_create_system(int ndim, int radius, an5d_shape shape, int n_fie
     }
 }
 
+an5d_status an5d_comm_unique_id(void* out128) {
+    if (!out128) return fail(AN5D_ERR_INVALID_ARGUMENT, "out is NULL");
+    const NcclApi& api = nccl();
+    if (!api.ok) return fail(AN5D_ERR_NCCL, "%s", api.why.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(out128, &id, sizeof(id));
+    return AN5D_OK;
+}
+
+an5d_status an5d_set_comm(an5d_plan* p, const void* nccl_unique_id, int rank, int nranks, int64_t global_outer_extent,
+                          int64_t outer_offset, int ghost_planes) {
+    try {
+        if (!p) return fail(AN5D_ERR_INVALID_ARGUMENT, "plan is NULL");
+        if (p->comm) {   // detach the previous communicator (stream-ordered work must be done)
+            if (p->comm_stream) cudaStreamSynchronize(p->comm_stream);
+            nccl().CommDestroy(p->comm);
+            p->comm = nullptr;
+        }
+        if (p->comm_stream) { cudaStreamDestroy(p->comm_stream); p->comm_stream = nullptr; }
+        if (p->ev_bnd) { cudaEventDestroy(p->ev_bnd); p->ev_bnd = nullptr; }
+        if (p->ev_xchg) { cudaEventDestroy(p->ev_xchg); p->ev_xchg = nullptr; }
+        p->rank = 0; p->nranks = 1; p->ghost = 0; p->gE0 = 0; p->outer_offset = 0;
+        if (!nccl_unique_id) return AN5D_OK;
+        if (nranks < 1 || rank < 0 || rank >= nranks) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad rank / nranks");
+        if (ghost_planes < 0 || global_outer_extent < 2 * p->rad + 1 || outer_offset < 0)
+            return fail(AN5D_ERR_INVALID_ARGUMENT, "bad ghost_planes / global_outer_extent / outer_offset");
+        if (p->nf > 1) return fail(AN5D_ERR_UNSUPPORTED, "slab mode: single-field plans only");
+        const NcclApi& api = nccl();
+        if (!api.ok) return fail(AN5D_ERR_NCCL, "%s", api.why.c_str());
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = api.CommInitRank(&comm, nranks, id, rank);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+        cudaError_t e;
+        if ((e = cudaStreamCreateWithFlags(&p->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&p->ev_bnd, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&p->ev_xchg, cudaEventDisableTiming)) != cudaSuccess) {
+            api.CommDestroy(comm);
+            return cuda_fail(e, "comm stream / events");
+        }
+        p->comm = comm;
+        p->rank = rank; p->nranks = nranks; p->ghost = ghost_planes;
+        p->gE0 = global_outer_extent; p->outer_offset = outer_offset;
+        return AN5D_OK;
+    } catch (...) {
+        return fail(AN5D_ERR_INVALID_ARGUMENT, "unexpected exception");
+    }
+}
+
 an5d_status an5d_destroy(an5d_plan* p) {
     if (!p) return AN5D_OK;
+    an5d_set_comm(p, nullptr, 0, 1, 0, 0, 0);   // releases a communicator, if any
     if (p->ctr) cudaFree(p->ctr);
     for (auto& kv : p->runs) cudaFree(kv.second.first);
     delete p;
@@ -1438,6 +1632,10 @@ an5d_status an5d_run(an5d_plan* p, void* grid_in, void* grid_out, const int64_t*
         if (T == 0) return launch_copy(*p, grid_in, grid_out, dm, false, 0, dm.E[0], st);
         an5d_config c{};
         if ((s = resolve_config(*p, dm, T, cfg, c)) != AN5D_OK) return s;
+        if (p->comm) {   // NCCL slab mode (an5d_set_comm)
+            if ((s = ensure_streams(*p)) != AN5D_OK) return s;
+            return run_comm(*p, grid_in, grid_out, dm, T, c, st);
+        }
         std::vector<int> deg;
         bool tc = false;
         make_schedule(T, c.bT, deg, tc);

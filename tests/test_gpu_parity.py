@@ -161,6 +161,29 @@ def test_gradient2d_bit_identical(an5d, dtype):
         assert not w.any(), cfg
 
 
+@pytest.mark.parametrize("name,dtype", [("star2d2r", torch.float32), ("star3d1r", torch.float64)])
+def test_set_comm_single_rank(an5d, name, dtype):
+    """an5d_set_comm: the library creates its own NCCL communicator; with one
+    rank the slab is the whole array and the run is bit-identical to a plain run; detaching
+    restores plain runs."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    ref, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, 11, dtype, {"bT": 2})
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    st.set_comm(an5d.comm_unique_id(), 0, 1, ext[0], 0, 0)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, dtype)
+    st.run(a, b, 11, {"bT": 2})
+    torch.cuda.synchronize()
+    assert np.array_equal(b.cpu().numpy(), ref)
+    st.set_comm(None)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    st.run(a, b, 11, {"bT": 2})
+    torch.cuda.synchronize()
+    assert np.array_equal(b.cpu().numpy(), ref)
+
+
 CLUSTER_CASES = [("star3d1r", torch.float32, 4, 256, (2, 4)), ("star3d2r", torch.float32, 2, 256, (2,)),
                  ("box3d1r", torch.float32, 2, 256, (2,)), ("j3d27pt", torch.float32, 2, 256, (2,)),
                  ("star3d1r", torch.float64, 3, 256, (2,)), ("star3d1r", torch.float64, 3, 512, (2,)),
