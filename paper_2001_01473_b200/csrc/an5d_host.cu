@@ -633,7 +633,10 @@ an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src,
     const cuuint64_t dims[3] = {(cuuint64_t)(dm.E[2] + x_off), (cuuint64_t)dm.E[1], (cuuint64_t)dm.E[0]};
     const cuuint64_t strides[2] = {(cuuint64_t)(dm.pitch[1] * p.elem), (cuuint64_t)(dm.pitch[0] * p.elem)};
     // one block's plane: a cluster layout's blocks each load their own tile_y / cluster rows
-    const cuuint32_t box[3] = {(cuuint32_t)inst.tile_x_loaded, (cuuint32_t)(inst.tile_y / std::max(1, inst.cluster)), 1};
+    // (a cluster layout's block also stages rad pad rows above and below: kernel3d.cuh kBoxRows)
+    const int cl = std::max(1, inst.cluster);
+    const cuuint32_t box[3] = {(cuuint32_t)inst.tile_x_loaded,
+                               (cuuint32_t)(inst.tile_y / cl + (cl > 1 ? 2 * p.rad : 0)), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(&tm, p.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                         reinterpret_cast<void*>(aligned), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

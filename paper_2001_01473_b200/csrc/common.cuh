@@ -144,6 +144,14 @@ __device__ __forceinline__ unsigned cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// split-phase cluster barrier: arrive (release: this thread's prior shared-memory writes become
+// visible to the cluster) ... independent work ... wait (acquire)
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 // generic address of the same shared-memory location in CTA `rank` of the cluster (DSMEM):
 // ordinary loads through it read the peer's shared memory
 template <typename T>

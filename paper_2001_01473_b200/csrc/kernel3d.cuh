@@ -150,9 +150,18 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                                              const Unit3D& g, const void* tmap, const unsigned crank = 0) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX_>;
     static_assert(CL == 1 || !K::XPLANE, "cluster halo sharing needs rad <= VY (row-band exchange)");
-    // block barrier (CL = 1) or cluster barrier (CL > 1)
+    // Cluster synchronisation.  Every block stages R extra rows above and below its window (the
+    // TMA box is kTY + 2R rows), so level 1 never reads a neighbour; levels >= 2 read the
+    // neighbours' exchange buffers.  With the level skew (SK, one exchange per step) the cluster
+    // barrier is SPLIT: arrive right after a step's publish (before its global stores), wait at
+    // the next step's start -- the stores and the TMA wait overlap the barrier latency (a joined
+    // release barrier per step waited for the step's stores and measured 2x slower, r02e).
+    // Without the skew (b_T >= 2) each level's exchange takes a full cluster barrier; b_T = 1 has
+    // no exchange at all (block barriers only).
+    constexpr bool CSPLIT = CL > 1 && K::SK && !(BOX && R >= 2);
+    constexpr bool CFULL = CL > 1 && !CSPLIT && BT >= 2;
     auto block_sync = [&]() {
-        if constexpr (CL > 1) cluster_sync_all();
+        if constexpr (CFULL) cluster_sync_all();
         else __syncthreads();
     };
     [[maybe_unused]] const bool peer_up = CL > 1 && crank > 0;          // block above in the cluster
@@ -222,13 +231,15 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // Planes outside [s_a, s_b) are not loaded (they feed nothing that is stored or pinned): the
     // slot's barrier is completed by a plain arrive.
     uint64_t* const mbar = reinterpret_cast<uint64_t*>(smem + (size_t)D * K::PLANE + (size_t)K::NXB * K::XBUF);
-    constexpr unsigned kBoxBytes = (unsigned)(K::kTX * K::kTY * sizeof(T));
+    // box rows: kTY (+ the R pad rows above and below with clusters: level 1 stays local)
+    constexpr int kBoxRows = K::kTY + (CL > 1 ? 2 * R : 0);
+    constexpr unsigned kBoxBytes = (unsigned)(K::kTX * kBoxRows * sizeof(T));
     auto issue_plane = [&](int64_t q, int slot) {
         if (tid == 0) {
             if (q >= g.s_a && q < g.s_b) {
                 mbar_arrive_expect_tx(mbar + slot, kBoxBytes);
-                tma_load_3d(stage + (size_t)slot * K::PLANE + R * kTX, tmap, g.wx0 + a.x_off, g.wy0, (int)q,
-                            mbar + slot);
+                tma_load_3d(stage + (size_t)slot * K::PLANE + (CL > 1 ? 0 : R * kTX), tmap, g.wx0 + a.x_off,
+                            g.wy0 - (CL > 1 ? R : 0), (int)q, mbar + slot);
             } else {
                 mbar_arrive(mbar + slot);
             }
@@ -282,6 +293,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     __syncthreads();
 #pragma unroll
     for (int d = 0; d < PF; ++d) issue_plane(base0 + d, d);
+    if constexpr (CSPLIT) cluster_arrive();   // phase 0: matched by the first step's wait
 
     // pin plane qi (relative index) of a patch to its original ring values, read from the stage
     auto pin = [&](E (&u)[VY][NE], int qi) {
@@ -350,7 +362,8 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
             const int64_t s = base + k;
             const int si = i;
             wait_plane(slot_i);                                // plane s has landed (TMA, mbarrier)
-            block_sync();                                      // ... and every thread (of the cluster) is past step s-1
+            if constexpr (CSPLIT) cluster_wait();              // ... every thread of the cluster published step s-1
+            else block_sync();                                 // ... and every thread is past step s-1
             {
                 int ns = slot_i + PF;
                 if (ns >= D) ns -= D;
@@ -379,17 +392,9 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
                     for (int yy = 0; yy < VY; ++yy) load_row(u0[yy], cur + own + yy * kTX);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        // cluster: rows owned by the block above / below come from its staged plane
-                        // (same slot: both blocks stream the same planes in lockstep)
-                        if (CL > 1 && tyi == 0 && peer_up)
-                            load_row_peer(yh_lo[r], cur + (K::kTY + r) * kTX + xs, crank - 1);
-                        else
-                            load_row(yh_lo[r], cur + own + (r - R) * kTX);
-                        if (CL > 1 && tyi == K::TYT - 1 && peer_dn)
-                            load_row_peer(yh_hi[r], cur + (R + r) * kTX + xs, crank + 1);
-                        else
-                            load_row(yh_hi[r], cur + own + (VY + r) * kTX);
+                    for (int r = 0; r < R; ++r) {   // (clusters: the staged pad rows are real rows)
+                        load_row(yh_lo[r], cur + own + (r - R) * kTX);
+                        load_row(yh_hi[r], cur + own + (VY + r) * kTX);
                     }
                 } else if constexpr (SK) {
                     // halo rows of level L-1's plane of the previous step, exchanged at its end
@@ -590,6 +595,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                     publish(xch + (size_t)(wb * (BT - 1) + (l - 1)) * K::XBUF, done);
                 });
                 xb = wb;
+                if constexpr (CSPLIT) cluster_arrive();   // published: the neighbours may read it next step
             }
             // ---- STORE level BT plane p = s - (BT-1) DL - R, compute region only --------------------
             const int pi = si - (BT - 1) * DL - R;
@@ -663,7 +669,8 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
         if (++slot_i == D) slot_i = 0;
     }
     // cluster: no block may exit (releasing its shared memory) while a neighbour can still read it
-    if constexpr (CL > 1) cluster_sync_all();
+    if constexpr (CSPLIT) cluster_wait();
+    else if constexpr (CFULL) cluster_sync_all();
 }
 
 // resident blocks per SM the register budget is shaped for: small fp32 patches (VY <= 2) fit two

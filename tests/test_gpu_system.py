@@ -100,15 +100,23 @@ def test_decoupled_system_equals_single_field_runs(an5d, dtype):
     tab[1, 0] = 0
     f = inputs.system_fields(21, nf, EXT)
     st = an5d.System(ndim, rad, shape, tab, dtype)
+    s1s = [an5d.Stencil(ndim, rad, shape, tab[i, i], 1.0, dtype) for i in range(nf)]
+    n_checked = 0
     for cfg in configs(an5d, st, EXT):
+        try:   # the single-field build may lack this (b_T, vec)
+            s1s[0].describe(EXT, cfg)
+        except an5d.AN5DError:
+            continue
+        n_checked += 1
         got, _ = run_system(an5d, ndim, rad, shape, tab, f, 9, dtype, cfg)
         for i in range(nf):
-            s1 = an5d.Stencil(ndim, rad, shape, tab[i, i], 1.0, dtype)
+            s1 = s1s[i]
             a = an5d.to_grid(torch.from_numpy(f[i].astype(NP[dtype])).cuda(), rad)
             b = an5d.empty_grid(EXT, rad, dtype)
             s1.run(a, b, 9, cfg)
             torch.cuda.synchronize()
             assert np.array_equal(got[i], b.cpu().numpy()), (cfg, i)
+    assert n_checked > 0
 
 
 @pytest.mark.parametrize("name", sorted(inputs.SYSTEMS))
