@@ -78,6 +78,7 @@ struct Plan {
     std::map<std::vector<int64_t>, std::pair<int4*, int64_t>> runs;
 };
 constexpr int kCtrRing = 64;            // counter pairs in flight per plan (>= concurrent sweeps)
+constexpr int kScratch2D = 1024 * 32;   // Sweep2DArgs::scratch slots
 constexpr size_t kRunCache = 64;        // run tables kept per plan
 
 }  // namespace an5d
@@ -603,8 +604,10 @@ an5d_status ensure_streams(Plan& p) {
     if (p.ctr) cudaFree(p.ctr);
     for (auto& kv : p.runs) cudaFree(kv.second.first);
     p.runs.clear();
-    if ((e = cudaMalloc(&p.ctr, sizeof(unsigned long long) * 2 * kCtrRing)) != cudaSuccess) return cuda_fail(e, "counter");
-    if ((e = cudaMemset(p.ctr, 0, sizeof(unsigned long long) * 2 * kCtrRing)) != cudaSuccess) return cuda_fail(e, "counter");
+    // counter pairs + the scratch slots of the 2D kernels' no-op lane atomics (kScratch2D)
+    const size_t n = 2 * kCtrRing + kScratch2D;
+    if ((e = cudaMalloc(&p.ctr, sizeof(unsigned long long) * n)) != cudaSuccess) return cuda_fail(e, "counter");
+    if ((e = cudaMemset(p.ctr, 0, sizeof(unsigned long long) * n)) != cudaSuccess) return cuda_fail(e, "counter");
     p.device = dev;
     return AN5D_OK;
 }
@@ -687,6 +690,7 @@ an5d_status launch_sweep(Plan& p, const void* src, void* dst, const Dims& dm, in
         a.Ey = dm.E[0]; a.g_off = g_off; a.gEy = gE0; a.out_lo = out_lo; a.out_hi = out_hi;
         a.h = g.h; a.n_units = g.n_units; a.n_sb = g.n_sb;
         a.ctr = p.ctr + 2 * (p.ctr_seq++ % kCtrRing);
+        a.scratch = p.ctr + 2 * kCtrRing;
         a.wc = wc; a.Ex = (int)dm.E[1]; a.C = g.C[0]; a.H = g.halo[0]; a.n_tiles_x = (int)g.ntiles[0];
         a.fstride = dm.fstride;
         set_peers(a, peers, dm.pitch[0], out_lo, out_hi);

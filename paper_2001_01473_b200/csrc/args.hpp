@@ -18,6 +18,7 @@ struct Sweep2DArgs {
     int64_t h;            // stream-block length h_SN
     int64_t n_units;      // (tile, stream block) units of this sweep
     unsigned long long* ctr;  // dynamic unit counter pair {next, finished blocks}; zero on entry
+    unsigned long long* scratch;  // 1024 x 32 zero slots: the other lanes' no-op atomics (kernel2d.cuh)
     int64_t n_sb;         // stream blocks
     int32_t* wc;          // debug: per-cell store counts (local Ey x Ex, dense), or nullptr
     long long* unit_ns;   // debug: per-unit (start, end, smid) globaltimer stamps, or nullptr
