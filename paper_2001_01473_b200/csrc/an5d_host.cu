@@ -159,7 +159,7 @@ int max_bT_for(const Plan& p, int vec) {
     int m = 0;
     for (const Instance& i : registry())
         if (i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad &&
-            i.vec == vec)
+            i.vec == vec && std::max(1, i.nf) == p.nf)
             m = std::max(m, i.bT);
     return m;
 }
@@ -463,7 +463,9 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
     std::vector<std::pair<double, an5d_config>> out;
     const int64_t Iout = dm.E[0] - 2 * p.rad;
     for (const Instance& inst : registry()) {
-        if (inst.ndim != p.ndim || inst.shape != p.shape || inst.dtype != p.dtype || inst.rad != p.rad) continue;
+        if (inst.ndim != p.ndim || inst.shape != p.shape || inst.dtype != p.dtype || inst.rad != p.rad ||
+            std::max(1, inst.nf) != p.nf)
+            continue;
         // gradient2d is non-associative: direct gather only
         const int direct = p.shape == AN5D_GRADIENT ? 1 : (hint ? hint->direct : 0);
         if (inst.assoc != (direct ? 0 : 1)) continue;
