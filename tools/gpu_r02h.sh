@@ -4,6 +4,7 @@
 #   3D suite at the planner's pick, ncu --set full of the 3D fp64 star sweeps and box3d4r fp32.
 TAG=${1:-r02h}
 mkdir -p gpurun_out
+timeout 600 python -m pytest tests -m gpu -q -k "edge_cases or decoupled or set_comm" > gpurun_out/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.txt
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:an5d_sweep -s 4 -c 1 -o gpurun_out/${TAG}_prof_headline \
