@@ -198,8 +198,6 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     const int tid = threadIdx.x;
     const int txi = tid % K::TXT, tyi = tid / K::TXT;
     const int xs = txi * VX, ys = tyi * VY;             // patch origin in the tile window
-    constexpr int kWarpRows = (32 / K::TXT) * VY;       // window rows of one warp
-    const int warp_y0 = (tid / 32) * kWarpRows;         // this warp's first window row
     const int gy0 = g.wy0 + ys, gx0 = g.wx0 + xs;       // this thread's first cell (array coords)
     T* const stage = smem;                              // D planes of PROWS x kTX
     T* const xch = smem + (size_t)D * K::PLANE;         // 2 exchange buffers
@@ -422,13 +420,6 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 auto rowref = [&](int yr) -> const E (&)[NE] {
                     return yr < 0 ? yh_lo[yr + R] : (yr >= VY ? yh_hi[yr - VY] : u[yr]);
                 };
-                // Dead warps: level L is only needed on rows at least L rad from the window's y
-                // edges (the valid region shrinks by rad per level and nothing outside
-                // it is stored or read by a valid cell).  A warp whose rows all lie outside skips
-                // the level's taps (warp-uniform branch) -- e.g. box3d4r: 2 of 8 warps at b_T = 1.
-                // Not with clusters (their inner block edges are not tile edges).
-                const bool dead_ = CL == 1 && (warp_y0 + kWarpRows <= L * R || warp_y0 >= K::kTY - L * R);
-                if (!dead_) {
                 constexpr int XR = BOX ? VY + 2 * R : VY;       // rows needing an x halo
                 T hl[XR][R], hh[XR][R];
 #pragma unroll
@@ -592,7 +583,6 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                         for (int dy = 1; dy <= R; ++dy) tap(C(dy, 0), dy, 0, false);
                     }
                 });
-                }
             });
             if constexpr (SK) {
                 // completed planes of levels 1..b_T-1: pin (ring), then publish their halo rows for
