@@ -124,7 +124,8 @@ typedef struct {
  *     [-r, r]; entry (d) multiplies the neighbour at offset +d: new[x] = sum_d c_d * old[x+d].
  *     STAR tables must have 0 on every entry with more than one non-zero offset component.
  *   divisor: 1.0 = none; j-stencils (j2d5pt, j2d9pt, j3d27pt) divide the sum by c_0 (Table 2).
- *     GRADIENT: c_0, the constant under the square root (any finite value, not folded).
+ *     GRADIENT: c_0, the constant under the square root, not folded; it must be finite and
+ *     >= the dtype's smallest normal number (FLT_MIN / DBL_MIN), else AN5D_ERR_UNSUPPORTED.
  *     Applied as in the paper's fast-math build: 1/c_0 is folded into
  *     the coefficients.  Each folded tap is one of the two dtype neighbours of c_d / c_0, chosen
  *     so that the taps' sum is as close as possible to sum_d c_d / c_0 (compensated rounding,

@@ -1099,6 +1099,10 @@ an5d_status an5d_create(int ndim, int radius, an5d_shape shape, const double* co
             return fail(AN5D_ERR_INVALID_ARGUMENT, "bad shape");
         if (shape == AN5D_GRADIENT && (ndim != 2 || radius != 1))
             return fail(AN5D_ERR_UNSUPPORTED, "gradient2d is ndim 2, radius 1 (Table 2 P:698-699)");
+        // gradient2d: c_0 + (sum of squares) must stay a normal number for the kernel's
+        // branch-free correctly rounded 1/sqrt (kernel2d.cuh rn_rsqrt_div)
+        if (shape == AN5D_GRADIENT && !(divisor >= (dtype == AN5D_F32 ? 1.1754943508222875e-38 : 2.2250738585072014e-308)))
+            return fail(AN5D_ERR_UNSUPPORTED, "gradient2d needs c_0 >= the dtype's smallest normal number");
         if (dtype != AN5D_F32 && dtype != AN5D_F64) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad dtype");
         if (!coeffs) return fail(AN5D_ERR_INVALID_ARGUMENT, "coeffs is NULL");
         if (!(divisor != 0.0) || !std::isfinite(divisor)) return fail(AN5D_ERR_INVALID_ARGUMENT, "bad divisor");
