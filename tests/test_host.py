@@ -181,6 +181,52 @@ def test_create_rejects_bad_arguments(an5d):
     with pytest.raises(an5d.AN5DError) as e:
         an5d.Stencil(2, 1, an5d.GRAD, off, 1.0, torch.float32)
     assert e.value.status == 4
+    cen = np.zeros((3, 3))
+    cen[1, 1] = 0.5
+    for c0 in (0.0, -1.0, 1e-39, float("inf")):   # c_0 must be a normal number (branch-free 1/sqrt)
+        with pytest.raises(an5d.AN5DError) as e:
+            an5d.Stencil(2, 1, an5d.GRAD, cen, c0, torch.float32)
+        assert e.value.status in (1, 5), c0
+    an5d.Stencil(2, 1, an5d.GRAD, cen, 1.0, torch.float32)
+
+
+def test_create_system_rejects_bad_arguments(an5d):
+    """an5d_create_system (multi-field systems, NEXT N4): block count, STAR off-axis entries in any
+    block, 3D with several fields, field count -- all rejected before anything runs."""
+    import numpy as np
+    import torch
+    import inputs
+    tab = inputs.system_table(2, 1, inputs.STAR, 2, seed=1)
+    an5d.System(2, 1, inputs.STAR, tab, torch.float32)
+    with pytest.raises(ValueError):
+        an5d.System(2, 1, inputs.STAR, tab[:1], torch.float32)           # not (n_f, n_f, ...)
+    bad = tab.copy()
+    bad[1, 0, 0, 0] = 0.25                                               # STAR off-axis, block (1, 0)
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.System(2, 1, inputs.STAR, bad, torch.float32)
+    assert e.value.status == 4
+    t3 = np.zeros((2, 2, 3, 3, 3))
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.System(3, 1, inputs.BOX, t3, torch.float32)
+    assert e.value.status == 5
+    with pytest.raises(an5d.AN5DError) as e:
+        an5d.System(2, 1, inputs.BOX, np.zeros((9, 9, 3, 3)), torch.float32)
+    assert e.value.status == 1
+
+
+def test_set_comm_argument_errors(an5d):
+    """an5d_set_comm: bad rank / nranks are rejected before NCCL is touched; detaching a plan that
+    has no communicator is a no-op."""
+    import numpy as np
+    import torch
+    import inputs
+    ndim, rad, shape, tab, div = inputs.benchmark_problem("star2d1r")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, torch.float32)
+    st.set_comm(None)
+    for rank, nranks in ((0, 0), (2, 2), (-1, 2)):
+        with pytest.raises(an5d.AN5DError) as e:
+            st.set_comm(b"\0" * 128, rank, nranks, 100, 0, 2)
+        assert e.value.status == 1
 
 
 def test_flops_per_cell_table2():
