@@ -76,15 +76,22 @@ CORE_LAYOUTS = {
     (3, 1, 1, 1): [(2, 2, "t32x2"), (2, 2, "c2t32x2")],
     (3, 0, 0, 1): [(2, 4, "c2"), (2, 4, "c4")], (3, 0, 0, 2): [(2, 2, "c2")], (3, 0, 1, 1): [(2, 2, "c2")],
 }
+# "os" = output-stationary b_T = 1 tiles (kernel3d.cuh OS): threads cover only the compute region,
+# neighbours are read from the staged plane (no halo cell computed, no shuffle) -- for the
+# stencils whose planner pick is b_T = 1 (high radius, high-order box, fp64 box rad 1)
+for _k in [(3, d, sh, r) for d in (0, 1) for sh in (0, 1) for r in (1, 2, 3, 4)
+           if (sh == 1 or r >= 2) and not (d == 0 and sh == 1 and r == 1)]:
+    CORE_LAYOUTS.setdefault(_k, []).append((2, 1, "os"))
 # fp32 128-wide tiles: measured 5-15 % slower than two 64-wide blocks per SM (r02b suite), never
 # picked by the tuner -> full build only
 FULL_LAYOUTS = {
     (3, 0, 0, 1): [(2, 4, "t32x4")], (3, 0, 0, 2): [(2, 2, "t32x4")], (3, 0, 0, 3): [(2, 1, "t32x4")],
     (3, 0, 0, 4): [(2, 1, "t32x4")], (3, 0, 1, 1): [(2, 2, "t32x4")],
 }
-# 3D layout -> (TXT, VX, CL): threads along x, cells per thread along x, blocks per cluster along y
+# 3D layout -> (TXT, VX, CL[, OS]): threads along x, cells per thread along x, blocks per cluster
+# along y, output-stationary b_T = 1 tiles
 LAYOUTS = {"": (16, 4, 1), "t32x2": (32, 2, 1), "t32x4": (32, 4, 1), "c2": (16, 4, 2), "c4": (16, 4, 4),
-           "c2t32x2": (32, 2, 2)}
+           "c2t32x2": (32, 2, 2), "os": (16, 4, 1, 1)}
 # 2D level split "w2" (kernel2d.cuh Split2D): two warps per tile, warp 0 levels 1..b_T/2 with the
 # staging, warp 1 the rest with the store -- half the partial-sum registers per warp.  b_T 1 has
 # nothing to split: the reduced-degree sweep of degree 1 uses the one-warp instance.
@@ -195,7 +202,8 @@ def generate():
         elif layout == "x2":
             targs += ", true, 1, false, 2"   # NF = 2 fields
         elif layout:
-            targs += ", %d, %d, %d" % LAYOUTS[layout]
+            lay = LAYOUTS[layout]
+            targs += ", %d, %d, %d" % lay[:3] + (", true" if len(lay) > 3 and lay[3] else "")
         fn = "make_instance2d" if ndim == 2 else "make_instance3d"
         lines = ["// GENERATED by paper_2001_01473_b200/build.py -- one kernel instance."]
         if name in caps:

@@ -6,10 +6,10 @@
 
 namespace an5d {
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX, int CL = 1>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX, int CL = 1, bool OS = false>
 cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap& tmap, int64_t blocks,
                      cudaStream_t st) {
-    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
     constexpr int N = (2 * R + 1) * (2 * R + 1) * (2 * R + 1);
     Coeffs3D<T, R> cf;
     const T* c = static_cast<const T*>(coeffs);
@@ -22,7 +22,7 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
         if constexpr (sizeof(T) == 4) cf.c[N + r] = make_float2(c[r * W + R + 1], c[r * W + R - 1]);
         else cf.c[N + r] = 0;
     }
-    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL>;
+    auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL, OS>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (!attr_set) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
@@ -50,19 +50,19 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
     return cudaGetLastError();
 }
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1, bool OS = false>
 Instance make_instance3d() {
-    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
     Instance i{};
     i.ndim = 3; i.shape = BOX ? 1 : 0; i.dtype = sizeof(T) == 8 ? 1 : 0;
     i.rad = R; i.bT = BT; i.vec = VY; i.assoc = 1;
     i.launch2d = nullptr;
-    i.launch3d = &launch3d<T, R, BT, VY, BOX, TXT, VX, CL>;
-    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL>);
+    i.launch3d = &launch3d<T, R, BT, VY, BOX, TXT, VX, CL, OS>;
+    i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL, OS>);
     i.fn_edge = i.fn_interior;
     i.threads = K::kThreads;
-    i.tile_x_loaded = K::kTX;
-    i.tile_y = K::kTY * CL;    // a cluster's blocks form one tile of CL x kTY rows
+    i.tile_x_loaded = K::kTXL;   // loaded width (output-stationary: compute width + 2 x halo)
+    i.tile_y = K::kTYL * CL;   // a cluster's blocks form one tile of CL x kTY rows (OS: + 2 rad halo rows)
     i.cluster = CL;
     i.smem_bytes = K::kSmemBytes;
     return i;

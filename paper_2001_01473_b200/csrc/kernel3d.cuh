@@ -47,23 +47,32 @@ constexpr int kPrefetch3D = 3;
 //                       so twice the warps per SM (one 16-byte vector per patch row);
 //   TXT_ = 32, VX_ = 4: 512 threads, 128 x 16 VY tile -- a wider tile: less x-halo redundancy
 //                       (the planner's b_S choice).
-template <typename T, int R, int BT, int VY, int TXT_ = 16, int VX_ = 4>
+//   OS_ = true ("output-stationary", b_T = 1 only): the threads cover only the COMPUTE region
+//                       (kTX x kTY cells); the TMA box adds the halo (HXO cells left/right, rad
+//                       rows above/below) and every thread reads its x and y neighbours straight
+//                       from the staged plane -- no halo cell is computed, no shuffle is needed.
+template <typename T, int R, int BT, int VY, int TXT_ = 16, int VX_ = 4, bool OS_ = false>
 struct Kernel3DTraits {
     static constexpr int VX = VX_;
     static constexpr int TXT = TXT_, TYT = 16;
-    static_assert(VX >= R, "x halo: a thread's rad neighbour cells must come from one adjacent thread");
+    static constexpr bool OS = OS_;
+    static_assert(OS || VX >= R, "x halo: a thread's rad neighbour cells must come from one adjacent thread");
     static_assert(VX % VecOf<T>::A == 0, "patch rows are whole 16-byte vectors");
+    static_assert(!OS || BT == 1, "output-stationary tiles are for b_T = 1");
     static constexpr int kThreads = TXT * TYT;
-    static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // tile plane (loaded), x by y
-    static constexpr int PROWS = kTY + 2 * R;               // staged rows (R garbage pad rows per side)
-    static constexpr int PLANE = PROWS * kTX;               // elements per staged plane
-    static constexpr int XROW = kTX;                        // exchange row (cells)
+    static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // thread window, x by y
+    static constexpr int HXO = OS ? ((R + VecOf<T>::A - 1) / VecOf<T>::A) * VecOf<T>::A : 0;  // OS x halo
+    static constexpr int kTXL = kTX + 2 * HXO;              // loaded / staged row (= kTX unless OS)
+    static constexpr int kTYL = kTY + (OS ? 2 * R : 0);     // loaded rows
+    static constexpr int PROWS = kTY + 2 * R;               // staged rows (R pad rows per side; OS: halo rows)
+    static constexpr int PLANE = PROWS * kTXL;              // elements per staged plane
+    static constexpr int XROW = kTXL;                       // exchange row (cells)
     // y-halo exchange: a thread publishes the rad rows its neighbours need (top and bottom rad rows
     // of its patch) -- possible while rad <= VY; otherwise (rad > VY) it publishes its whole patch
     // into a padded plane and reads rad rows spanning several threads above / below
     static constexpr bool XPLANE = R > VY;
     static constexpr int XBAND = 2 * R * XROW;              // exchange rows of one thread row
-    static constexpr int XBUF = XPLANE ? PROWS * kTX : (TYT + 2) * XBAND;  // one exchange buffer
+    static constexpr int XBUF = XPLANE ? PROWS * kTXL : (TYT + 2) * XBAND;  // one exchange buffer
     // Level skew SK (see sweep3d_unit): with SK = 1 level L at step s takes the plane level L-1
     // completed at step s-1, so all levels' halo rows are exchanged together behind the one
     // barrier a step has anyway (1 barrier per plane instead of b_T).  Costs deeper staging (the
@@ -145,10 +154,11 @@ using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * 
 // plane, level L >= 2 from its exchange buffer; the per-step block barrier becomes a cluster
 // barrier (release/acquire), which also orders the neighbour's reads against the reuse of its
 // stage slots and exchange buffers (both are double-buffered or D - PF >= 1 planes deep).
-template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_, int CL = 1>
+template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_, int CL = 1, bool OS = false>
 __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
                                              const Unit3D& g, const void* tmap, const unsigned crank = 0) {
-    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX_>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX_, OS>;
+    static_assert(!OS || CL == 1, "output-stationary tiles are not clustered");
     static_assert(CL == 1 || !K::XPLANE, "cluster halo sharing needs rad <= VY (row-band exchange)");
     // Cluster synchronisation.  Every block stages R extra rows above and below its window (the
     // TMA box is kTY + 2R rows), so level 1 never reads a neighbour; levels >= 2 read the
@@ -192,13 +202,13 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     constexpr int SK = (K::SK && !ROT) ? 1 : 0;
     // (a rotated-slot kernel runs unskewed inside the skewed traits' buffers: D1 >= D0, >= 2 buffers)
     constexpr int DL = R + SK;              // plane delay per level
-    constexpr int kTX = K::kTX;
+    constexpr int kTX = K::kTXL;   // staged row stride (the loaded width)
 
     T* __restrict__ dst = static_cast<T*>(a.dst);
     const int tid = threadIdx.x;
     const int txi = tid % K::TXT, tyi = tid / K::TXT;
-    const int xs = txi * VX, ys = tyi * VY;             // patch origin in the tile window
-    const int gy0 = g.wy0 + ys, gx0 = g.wx0 + xs;       // this thread's first cell (array coords)
+    const int xs = K::HXO + txi * VX, ys = tyi * VY;    // patch origin in the tile window (OS: past the x halo)
+    const int gy0 = g.wy0 + ys + (OS ? R : 0), gx0 = g.wx0 + xs;   // this thread's first cell (array coords)
     T* const stage = smem;                              // D planes of PROWS x kTX
     T* const xch = smem + (size_t)D * K::PLANE;         // 2 exchange buffers
     const int own = (ys + R) * kTX + xs;                // patch origin inside a staged plane
@@ -232,13 +242,13 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // slot's barrier is completed by a plain arrive.
     uint64_t* const mbar = reinterpret_cast<uint64_t*>(smem + (size_t)D * K::PLANE + (size_t)K::NXB * K::XBUF);
     // box rows: kTY (+ the R pad rows above and below with clusters: level 1 stays local)
-    constexpr int kBoxRows = K::kTY + (CL > 1 ? 2 * R : 0);
-    constexpr unsigned kBoxBytes = (unsigned)(K::kTX * kBoxRows * sizeof(T));
+    constexpr int kBoxRows = K::kTY + ((CL > 1 || OS) ? 2 * R : 0);
+    constexpr unsigned kBoxBytes = (unsigned)(K::kTXL * kBoxRows * sizeof(T));
     auto issue_plane = [&](int64_t q, int slot) {
         if (tid == 0) {
             if (q >= g.s_a && q < g.s_b) {
                 mbar_arrive_expect_tx(mbar + slot, kBoxBytes);
-                tma_load_3d(stage + (size_t)slot * K::PLANE + (CL > 1 ? 0 : R * kTX), tmap, g.wx0 + a.x_off,
+                tma_load_3d(stage + (size_t)slot * K::PLANE + ((CL > 1 || OS) ? 0 : R * kTX), tmap, g.wx0 + a.x_off,
                             g.wy0 - (CL > 1 ? R : 0), (int)q, mbar + slot);
             } else {
                 mbar_arrive(mbar + slot);
@@ -422,8 +432,29 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 };
                 constexpr int XR = BOX ? VY + 2 * R : VY;       // rows needing an x halo
                 T hl[XR][R], hh[XR][R];
+                if constexpr (OS) {
+                    // output-stationary (b_T = 1, level 1 = the staged plane): the rad cells left
+                    // and right of each row, read from the stage as whole 16-byte vectors
+                    constexpr int NVA = K::HXO;          // cells loaded per side (rad rounded to vectors)
+#pragma unroll
+                    for (int t = 0; t < XR; ++t) {
+                        const T* rowp = cur + own + (BOX ? t - R : t) * kTX;
+                        T lb[NVA], rb[NVA];
+#pragma unroll
+                        for (int j = 0; j < NVA; j += A) {
+                            ld_vec_shared<T>(lb + j, rowp - NVA + j);
+                            ld_vec_shared<T>(rb + j, rowp + VX + j);
+                        }
+#pragma unroll
+                        for (int m = 0; m < R; ++m) {
+                            hl[t][m] = lb[NVA - R + m];
+                            hh[t][m] = rb[m];
+                        }
+                    }
+                } else {
 #pragma unroll
                 for (int t = 0; t < XR; ++t) xhalo(rowref(BOX ? t - R : t), hl[t], hh[t]);
+                }
                 auto X = [&](int yr, int c) -> T {
                     const int t = BOX ? yr + R : yr;
                     return c < 0 ? hl[t][c + R] : (c >= VX ? hh[t][c - VX] : LN::cell(rowref(yr), c));
@@ -689,10 +720,10 @@ template <typename T, int VY, int R, bool BOX, int TXT> constexpr int min_blocks
 
 // CL > 1: launched with cluster dimension (CL, 1, 1); the CL consecutive blocks of a cluster take
 // the same unit (a cluster tile of CL x kTY rows) and block rank c its rows [c kTY, (c+1) kTY).
-template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1, bool OS = false>
 __global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
 an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
-    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX>;
+    using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* const smem = reinterpret_cast<T*>(smem_raw);
     const int64_t unit = blockIdx.x / CL;
@@ -717,7 +748,7 @@ an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, con
         const int cy0 = R + ty * a.Cy, cy1 = min(cy0 + a.Cy, a.Ey - R);
         g.wy0 = cy0 - a.Hy + (int)crank * K::kTY;
         g.cy0 = max(cy0, g.wy0);
-        g.cy1 = min(cy1, g.wy0 + K::kTY);   // may be empty (a block below the array end)
+        g.cy1 = min(cy1, g.wy0 + K::kTYL);  // may be empty (a block below the array end)
     }
     g.cx0 = R + tx * a.Cx;
     g.cx1 = min(g.cx0 + a.Cx, a.Ex - R);
@@ -728,14 +759,14 @@ an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, con
     g.s_end = g.p1 + (int64_t)BT * R;
     g.s_a = max(g.s_first, (int64_t)0);
     g.s_b = min(g.s_end, a.Ez);
-    g.ring_xy = g.wy0 < R || g.wy0 + K::kTY > a.Ey - R || g.wx0 < R || g.wx0 + K::kTX > a.Ex - R;
+    g.ring_xy = g.wy0 < R || g.wy0 + K::kTYL > a.Ey - R || g.wx0 < R || g.wx0 + K::kTXL > a.Ex - R;
     // z-ring planes and the array's z ends are handled by both variants (uniform per-step checks);
     // the EDGE variant is only for tiles whose window touches the x/y ring or the array end
     if (threadIdx.x == 0) tma_prefetch_desc(&tmap);
     // units storing planes of the fused-exchange send bands run the EDGE copy too
     if (g.ring_xy || (a.peer_lo && g.p0 < a.send_lo_end) || (a.peer_hi && g.p1 > a.send_hi_begin))
-        sweep3d_unit<T, R, BT, VY, BOX, true, TXT, VX, CL>(a, cf, smem, g, &tmap, crank);
-    else sweep3d_unit<T, R, BT, VY, BOX, false, TXT, VX, CL>(a, cf, smem, g, &tmap, crank);
+        sweep3d_unit<T, R, BT, VY, BOX, true, TXT, VX, CL, OS>(a, cf, smem, g, &tmap, crank);
+    else sweep3d_unit<T, R, BT, VY, BOX, false, TXT, VX, CL, OS>(a, cf, smem, g, &tmap, crank);
 }
 
 }  // namespace an5d
