@@ -65,7 +65,9 @@ struct Kernel3DTraits {
     static constexpr int kTXL = kTX + 2 * HXO;              // loaded / staged row (= kTX unless OS)
     static constexpr int kTYL = kTY + (OS ? 2 * R : 0);     // loaded rows
     static constexpr int PROWS = kTY + 2 * R;               // staged rows (R pad rows per side; OS: halo rows)
-    static constexpr int PLANE = PROWS * kTXL;              // elements per staged plane
+    // elements per staged plane, rounded to 128 bytes: every slot is a TMA destination, which must
+    // be 128-byte aligned (the output-stationary 72-wide rows broke that: misaligned address)
+    static constexpr int PLANE = ((PROWS * kTXL * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
     static constexpr int XROW = kTXL;                       // exchange row (cells)
     // y-halo exchange: a thread publishes the rad rows its neighbours need (top and bottom rad rows
     // of its patch) -- possible while rad <= VY; otherwise (rad > VY) it publishes its whole patch
