@@ -80,7 +80,7 @@ CORE_LAYOUTS = {
 # neighbours are read from the staged plane (no halo cell computed, no shuffle) -- for the
 # stencils whose planner pick is b_T = 1 (high radius, high-order box, fp64 box rad 1)
 for _k in [(3, d, sh, r) for d in (0, 1) for sh in (0, 1) for r in (1, 2, 3, 4)
-           if (sh == 1 or r >= 2) and not (d == 0 and sh == 1 and r == 1)]:
+           if sh == 1 or r >= 2]:
     CORE_LAYOUTS.setdefault(_k, []).append((2, 1, "os"))
 # fp32 128-wide tiles: measured 5-15 % slower than two 64-wide blocks per SM (r02b suite), never
 # picked by the tuner -> full build only

@@ -185,7 +185,8 @@ def test_set_comm_single_rank(an5d, name, dtype):
 
 
 OS_CASES = [(n, d) for n in ("star3d2r", "star3d3r", "star3d4r", "box3d2r", "box3d3r", "box3d4r")
-            for d in (torch.float32, torch.float64)] + [("box3d1r", torch.float64), ("j3d27pt", torch.float64)]
+            for d in (torch.float32, torch.float64)] + [(n, d) for n in ("box3d1r", "j3d27pt")
+                                                        for d in (torch.float32, torch.float64)]
 
 
 @pytest.mark.parametrize("name,dtype", OS_CASES)
