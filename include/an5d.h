@@ -90,6 +90,10 @@ typedef struct {
                      /* selects the layout: 2D 32 (one warp per tile); 3D 256 (16 x 16 threads, */
                      /* 64-wide tiles) or 512 (32 x 16 threads: 64-wide fp64 tiles at half the  */
                      /* registers per thread, or 128-wide fp32 tiles).  0 = planner / default.  */
+                     /* 3D bS[0] (the loaded tile height) also names the thread-block-cluster   */
+                     /* layouts (2 / 4 blocks stacked along y sharing y halos through DSMEM: 64 / */
+                     /* 128 rows) and, at b_T = 1, the output-stationary tiles (threads on the  */
+                     /* 64 x 32 compute region only: bS = {32 + 2 rad, 64 + 2 rad}).            */
 } an5d_config;
 
 /* Bookkeeping of one sweep of degree bT under `cfg` (bit-exact).        */
