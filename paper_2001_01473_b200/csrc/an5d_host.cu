@@ -1358,8 +1358,8 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         const int64_t launches0 = p->launches;
         // one warm-up sweep + two timed sweeps of a configuration: seconds per cell-step (1e300 if
         // it cannot run)
-        // one warm-up sweep, then timed sweeps for >= 15 ms (at least 2, at most 96); every candidate
-        // is timed in three passes (forward, backward, forward) and scored by its median pass: under
+        // one warm-up sweep, then timed sweeps for >= 20 ms (at least 2, at most 96); every candidate
+        // is timed in five passes (alternating forward / backward) and scored by its median pass: under
         // the 1 kW power cap the clocks drift by up to 10 % within a tune, which ordered short
         // single passes by the candidates' position rather than their speed (round-2 measurements)
         auto measure = [&](const an5d_config& c0, an5d_config& c) -> double {
@@ -1378,7 +1378,7 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             }
             float ms1 = 0;
             cudaEventElapsedTime(&ms1, e0, e1);
-            const int n = std::max(2, std::min(96, (int)std::ceil(15.0 / std::max(ms1, 1e-3f))));
+            const int n = std::max(2, std::min(96, (int)std::ceil(20.0 / std::max(ms1, 1e-3f))));
             cudaEventRecord(e0, st);
             for (int r = 0; r < n && ok; ++r) ok = sweep();
             cudaEventRecord(e1, st);
@@ -1411,19 +1411,22 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
             }
         }
         const bool tlog = getenv("AN5D_TUNE_LOG") != nullptr;   // debug: every candidate's time
-        // three passes (forward, backward, forward), each candidate scored by its median pass
+        // five passes (alternating forward / backward), each candidate scored by its median pass
+        // (three passes still flipped star2d1r between b_T 7 and 8 -- 5 % apart -- from run to run
+        // under the power cap, r02final/r02final2)
+        constexpr int kPasses = 5;
         std::vector<std::vector<double>> times(cand.size());
         std::vector<double> score(cand.size(), 1e300);
         std::vector<an5d_config> resolved(cand.size());
-        for (int pass = 0; pass < 3; ++pass)
+        for (int pass = 0; pass < kPasses; ++pass)
             for (size_t j = 0; j < cand.size(); ++j) {
-                const size_t q = pass == 1 ? cand.size() - 1 - j : j;
+                const size_t q = (pass & 1) ? cand.size() - 1 - j : j;
                 const double t = measure(cand[q], resolved[q]);
                 times[q].push_back(t);
-                if (times[q].size() == 3) {
+                if ((int)times[q].size() == kPasses) {
                     std::vector<double> v = times[q];
                     std::sort(v.begin(), v.end());
-                    score[q] = v[1];
+                    score[q] = v[kPasses / 2];
                 }
                 if (tlog)
                     fprintf(stderr, "an5d_tune: pass %d bT %d vec %d n_thr %d bS %d,%d h %lld -> %.4g ps/cell-step\n",
