@@ -267,8 +267,9 @@ def main():
     ap.add_argument("--direct", type=int, default=0, choices=[0, 1],
                     help="1 = partial sums OFF: the non-associative direct-gather kernels (BASELINE config 4)")
     ap.add_argument("--no-tune", action="store_true", help="planner model only (no measured top-5 pick)")
-    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
-                    help="N > 1: halo exchange by peer stores from the sweep kernels (fused, NEXT N1) or NCCL send/recv")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl", "lib"],
+                    help="N > 1: halo exchange by peer stores from the sweep kernels (fused, NEXT N1), NCCL "
+                         "send/recv from Python (nccl) or the library's own NCCL communicator (lib, an5d_set_comm)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-step-seconds", type=float, default=3.0)

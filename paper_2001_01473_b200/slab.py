@@ -397,7 +397,14 @@ def bench_main(args, workloads):
     b.copy_(a)
     comm = torch.cuda.Stream(dev)
     bufs = [a, b]
-    fused = getattr(args, "exchange", "fused") == "fused"
+    exchange = getattr(args, "exchange", "fused")
+    fused = exchange == "fused"
+    if exchange == "lib":
+        # the library's own NCCL communicator (an5d_set_comm): an5d_run does the whole slab run,
+        # ncclSend/ncclRecv of the ghost planes on a library comm stream
+        uid = [an5d.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        st.set_comm(uid[0], rank, ws, gext[0], s.loc_lo, s.G)
     if fused:
         # fused halo exchange (NEXT N1): peer-mapped ghost planes written by the sweep kernels
         flag = torch.zeros(32, dtype=torch.int32, device=dev)
@@ -411,6 +418,8 @@ def bench_main(args, workloads):
         if fused:
             run_fused(st, s, (src, dst), T, cfg, links if i % 2 == 0 else links_b,
                       stream=torch.cuda.current_stream(dev))
+        elif exchange == "lib":
+            st.run(src, dst, T, cfg)
         else:
             run_distributed(st, s, (src, dst), T, cfg, comm_stream=comm)
 
@@ -480,6 +489,8 @@ def bench_main(args, workloads):
                 # the e2e pairs are other buffers: the exchange for them goes through the NCCL
                 # runner (the fused links map the timed buffers a, b only)
                 run_distributed(st, s, (ga, gb), T, cfg, comm_stream=comm)
+            elif exchange == "lib":
+                st.run(ga, gb, T, cfg)
             else:
                 run_distributed(st, s, (ga, gb), T, cfg, comm_stream=comm)
             ev_comp[j].record(main)
@@ -533,7 +544,8 @@ def bench_main(args, workloads):
             "dtype": "f32" if dtype == torch.float32 else "f64", "data": "synthetic",
             "config": {"workload": args.workload, "stencil": name, "grid": list(gext), "T": T, "bT": cfg["bT"],
                        "vec": cfg["vec"], "h": cfg["h"], "n_thr": cfg.get("n_thr"),
-                       "parallelism": f"slab{ws} (outermost dim, " + ("fused peer-store halo exchange over NVLink)" if fused else "NCCL halo)"),
+                       "parallelism": f"slab{ws} (outermost dim, " + ("fused peer-store halo exchange over NVLink)" if fused else
+                                                                      ("library NCCL halo, an5d_set_comm)" if exchange == "lib" else "NCCL halo)")),
                        "planner": "model top-5, measured pick on rank 0 (P:784-793)" if tuned else "model",
                        "l2": "inputs larger than L2"},
             "gflops": round(gcells * F, 2), "roofline": rl, "cpu_baseline": None, "e2e": e2e,
