@@ -6,7 +6,7 @@
 
 namespace an5d {
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX, int CL = 1, bool OS = false>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT, int VX, int CL = 1, int OS = 0>
 cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap& tmap, int64_t blocks,
                      cudaStream_t st) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
@@ -50,7 +50,7 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
     return cudaGetLastError();
 }
 
-template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1, bool OS = false>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1, int OS = 0>
 Instance make_instance3d() {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
     Instance i{};

@@ -47,23 +47,29 @@ constexpr int kPrefetch3D = 3;
 //                       so twice the warps per SM (one 16-byte vector per patch row);
 //   TXT_ = 32, VX_ = 4: 512 threads, 128 x 16 VY tile -- a wider tile: less x-halo redundancy
 //                       (the planner's b_S choice).
-//   OS_ = true ("output-stationary", b_T = 1 only): the threads cover only the COMPUTE region
-//                       (kTX x kTY cells); the TMA box adds the halo (HXO cells left/right, rad
-//                       rows above/below) and every thread reads its x and y neighbours straight
-//                       from the staged plane -- no halo cell is computed, no shuffle is needed.
-template <typename T, int R, int BT, int VY, int TXT_ = 16, int VX_ = 4, bool OS_ = false>
+//   OS_ ("output-stationary" staging, bit flags):
+//     bit 0 (y): the TMA box adds rad rows above and below the thread window, so level 1 reads
+//                real rows there and the y halo the threads compute shrinks from b_T rad to
+//                (b_T - 1) rad (any b_T; levels >= 2 exchange rows as before);
+//     bit 1 (x, b_T = 1 only): the box also adds the x halo (HXO cells left/right) and every
+//                thread reads its x neighbours from the staged plane -- at b_T = 1 the threads
+//                then cover only the compute region (kTX x kTY cells): no halo cell is computed,
+//                no shuffle is needed.
+template <typename T, int R, int BT, int VY, int TXT_ = 16, int VX_ = 4, int OS_ = 0>
 struct Kernel3DTraits {
     static constexpr int VX = VX_;
     static constexpr int TXT = TXT_, TYT = 16;
-    static constexpr bool OS = OS_;
-    static_assert(OS || VX >= R, "x halo: a thread's rad neighbour cells must come from one adjacent thread");
+    static constexpr int OS = OS_;
+    static constexpr bool OSY = (OS & 1) != 0, OSX = (OS & 2) != 0;
+    static_assert(OSX || VX >= R, "x halo: a thread's rad neighbour cells must come from one adjacent thread");
+    static_assert(!OSX || OSY, "x staging implies y staging");
     static_assert(VX % VecOf<T>::A == 0, "patch rows are whole 16-byte vectors");
-    static_assert(!OS || BT == 1, "output-stationary tiles are for b_T = 1");
+    static_assert(!OSX || BT == 1, "output-stationary x staging is for b_T = 1");
     static constexpr int kThreads = TXT * TYT;
     static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // thread window, x by y
-    static constexpr int HXO = OS ? ((R + VecOf<T>::A - 1) / VecOf<T>::A) * VecOf<T>::A : 0;  // OS x halo
+    static constexpr int HXO = OSX ? ((R + VecOf<T>::A - 1) / VecOf<T>::A) * VecOf<T>::A : 0;  // staged x halo
     static constexpr int kTXL = kTX + 2 * HXO;              // loaded / staged row (= kTX unless OS)
-    static constexpr int kTYL = kTY + (OS ? 2 * R : 0);     // loaded rows
+    static constexpr int kTYL = kTY + (OSY ? 2 * R : 0);    // loaded rows
     static constexpr int PROWS = kTY + 2 * R;               // staged rows (R pad rows per side; OS: halo rows)
     // elements per staged plane, rounded to 128 bytes: every slot is a TMA destination, which must
     // be 128-byte aligned (the output-stationary 72-wide rows broke that: misaligned address)
@@ -156,7 +162,7 @@ using Coeffs3D = Coeffs<typename CoefElem<T>::type, (2 * R + 1) * (2 * R + 1) * 
 // plane, level L >= 2 from its exchange buffer; the per-step block barrier becomes a cluster
 // barrier (release/acquire), which also orders the neighbour's reads against the reuse of its
 // stage slots and exchange buffers (both are double-buffered or D - PF >= 1 planes deep).
-template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_, int CL = 1, bool OS = false>
+template <typename T, int R, int BT, int VY, bool BOX, bool EDGE, int TXT, int VX_, int CL = 1, int OS = 0>
 __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3D<T, R>& cf, T* const smem,
                                              const Unit3D& g, const void* tmap, const unsigned crank = 0) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX_, OS>;
@@ -210,7 +216,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     const int tid = threadIdx.x;
     const int txi = tid % K::TXT, tyi = tid / K::TXT;
     const int xs = K::HXO + txi * VX, ys = tyi * VY;    // patch origin in the tile window (OS: past the x halo)
-    const int gy0 = g.wy0 + ys + (OS ? R : 0), gx0 = g.wx0 + xs;   // this thread's first cell (array coords)
+    const int gy0 = g.wy0 + ys + (K::OSY ? R : 0), gx0 = g.wx0 + xs;   // this thread's first cell (array coords)
     T* const stage = smem;                              // D planes of PROWS x kTX
     T* const xch = smem + (size_t)D * K::PLANE;         // 2 exchange buffers
     const int own = (ys + R) * kTX + xs;                // patch origin inside a staged plane
@@ -244,13 +250,13 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // slot's barrier is completed by a plain arrive.
     uint64_t* const mbar = reinterpret_cast<uint64_t*>(smem + (size_t)D * K::PLANE + (size_t)K::NXB * K::XBUF);
     // box rows: kTY (+ the R pad rows above and below with clusters: level 1 stays local)
-    constexpr int kBoxRows = K::kTY + ((CL > 1 || OS) ? 2 * R : 0);
+    constexpr int kBoxRows = K::kTY + ((CL > 1 || K::OSY) ? 2 * R : 0);
     constexpr unsigned kBoxBytes = (unsigned)(K::kTXL * kBoxRows * sizeof(T));
     auto issue_plane = [&](int64_t q, int slot) {
         if (tid == 0) {
             if (q >= g.s_a && q < g.s_b) {
                 mbar_arrive_expect_tx(mbar + slot, kBoxBytes);
-                tma_load_3d(stage + (size_t)slot * K::PLANE + ((CL > 1 || OS) ? 0 : R * kTX), tmap, g.wx0 + a.x_off,
+                tma_load_3d(stage + (size_t)slot * K::PLANE + ((CL > 1 || K::OSY) ? 0 : R * kTX), tmap, g.wx0 + a.x_off,
                             g.wy0 - (CL > 1 ? R : 0), (int)q, mbar + slot);
             } else {
                 mbar_arrive(mbar + slot);
@@ -434,7 +440,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 };
                 constexpr int XR = BOX ? VY + 2 * R : VY;       // rows needing an x halo
                 T hl[XR][R], hh[XR][R];
-                if constexpr (OS) {
+                if constexpr (K::OSX) {
                     // output-stationary (b_T = 1, level 1 = the staged plane): the rad cells left
                     // and right of each row, read from the stage as whole 16-byte vectors
                     constexpr int NVA = K::HXO;          // cells loaded per side (rad rounded to vectors)
@@ -722,7 +728,7 @@ template <typename T, int VY, int R, bool BOX, int TXT> constexpr int min_blocks
 
 // CL > 1: launched with cluster dimension (CL, 1, 1); the CL consecutive blocks of a cluster take
 // the same unit (a cluster tile of CL x kTY rows) and block rank c its rows [c kTY, (c+1) kTY).
-template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1, bool OS = false>
+template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4, int CL = 1, int OS = 0>
 __global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
 an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;

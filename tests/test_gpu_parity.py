@@ -229,6 +229,47 @@ def test_output_stationary_bt1(an5d, name, dtype):
     assert not w.any()
 
 
+OY_CASES = [("star3d1r", torch.float32, 4, 256), ("star3d2r", torch.float32, 2, 256), ("box3d1r", torch.float32, 2, 256),
+            ("star3d1r", torch.float64, 3, 512), ("star3d2r", torch.float64, 2, 512), ("box3d1r", torch.float64, 2, 512)]
+
+
+@pytest.mark.parametrize("name,dtype,bmax,n_thr", OY_CASES)
+def test_y_staged_tiles(an5d, name, dtype, bmax, n_thr):
+    """y-staged tiles (kernel3d.cuh OS bit 0): the TMA box adds rad rows above and below, so the
+    threads' y halo shrinks to (b_T - 1) rad.  Bit-identical to the default layout at every b_T,
+    within tolerance of the oracle, exact-integer bit-identical, write counts once per sweep."""
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    gx = inputs.global_grid(1234, ext, kind="pm")
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    for bT in range(1, bmax + 1):
+        cfg = {"bT": bT, "vec": 2, "h": 8, "n_thr": n_thr, "bS": [32 + 2 * rad, 0]}
+        d = st.describe(ext, cfg)
+        assert d["bS_loaded"][0] == 32 + 2 * rad and d["compute"][0] == 32 - 2 * (bT - 1) * rad, d
+        for T in sorted({1, bT, 2 * bT + 3}):
+            got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+            ref, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, dict(cfg, bS=[32, 0]))
+            assert np.array_equal(got, ref), (name, bT, T)
+            exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+            assert ring_equal(got, exp, rad) and rel_linf(got, exp, rad) <= TOL[dtype], (name, bT, T)
+        T = _exact_T(ndim, rad, shape, 2 * bT + 3, dtype)
+        got, _ = gpu_run(an5d, ndim, rad, shape, tabx, divx, gx, T, dtype, cfg)
+        assert np.array_equal(got, oracle.run(gx, rad, shape, tabx, divx, T, NP[dtype])), (name, bT, T)
+        a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+        b = an5d.empty_grid(ext, rad, dtype)
+        wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+        st.copy_ring(a, b)
+        st.sweep(a, b, bT, cfg, write_count=wc)
+        torch.cuda.synchronize()
+        w = wc.cpu().numpy()
+        core = tuple(slice(rad, e - rad) for e in ext)
+        assert np.all(w[core] == 1), bT
+        w[core] = 0
+        assert not w.any(), bT
+
+
 CLUSTER_CASES = [("star3d1r", torch.float32, 4, 256, (2, 4)), ("star3d2r", torch.float32, 2, 256, (2,)),
                  ("box3d1r", torch.float32, 2, 256, (2,)), ("j3d27pt", torch.float32, 2, 256, (2,)),
                  ("star3d1r", torch.float64, 3, 256, (2,)), ("star3d1r", torch.float64, 3, 512, (2,)),
