@@ -86,8 +86,9 @@ for _k in [(3, d, sh, r) for d in (0, 1) for sh in (0, 1) for r in (1, 2, 3, 4)
 # shrinks from b_T rad to (b_T - 1) rad; the stencils whose pick is b_T >= 2 (fp64: the 512-thread
 # layout "oyt32x2")
 for _k, _lst in {(3, 0, 0, 1): [(2, 4, "oy")], (3, 0, 0, 2): [(2, 2, "oy")], (3, 0, 1, 1): [(2, 2, "oy")],
-                 (3, 1, 0, 1): [(2, 3, "oyt32x2")], (3, 1, 0, 2): [(2, 2, "oyt32x2")],
-                 (3, 1, 1, 1): [(2, 2, "oyt32x2")]}.items():
+                 (3, 1, 0, 1): [(2, 3, "oyt32x2"), (2, 3, "osxyt32x2")],
+                 (3, 1, 0, 2): [(2, 2, "oyt32x2"), (2, 2, "osxyt32x2")],
+                 (3, 1, 1, 1): [(2, 2, "oyt32x2"), (2, 2, "osxyt32x2")]}.items():
     CORE_LAYOUTS.setdefault(_k, []).extend(_lst)
 # fp32 128-wide tiles: measured 5-15 % slower than two 64-wide blocks per SM (r02b suite), never
 # picked by the tuner -> full build only
@@ -98,7 +99,8 @@ FULL_LAYOUTS = {
 # 3D layout -> (TXT, VX, CL[, OS]): threads along x, cells per thread along x, blocks per cluster
 # along y, output-stationary b_T = 1 tiles
 LAYOUTS = {"": (16, 4, 1), "t32x2": (32, 2, 1), "t32x4": (32, 4, 1), "c2": (16, 4, 2), "c4": (16, 4, 4),
-           "c2t32x2": (32, 2, 2), "os": (16, 4, 1, 3), "oy": (16, 4, 1, 1), "oyt32x2": (32, 2, 1, 1)}
+           "c2t32x2": (32, 2, 2), "os": (16, 4, 1, 3), "oy": (16, 4, 1, 1), "oyt32x2": (32, 2, 1, 1),
+           "osxyt32x2": (32, 2, 1, 3)}
 # 2D level split "w2" (kernel2d.cuh Split2D): two warps per tile, warp 0 levels 1..b_T/2 with the
 # staging, warp 1 the rest with the store -- half the partial-sum registers per warp.  b_T 1 has
 # nothing to split: the reduced-degree sweep of degree 1 uses the one-warp instance.

@@ -51,10 +51,11 @@ constexpr int kPrefetch3D = 3;
 //     bit 0 (y): the TMA box adds rad rows above and below the thread window, so level 1 reads
 //                real rows there and the y halo the threads compute shrinks from b_T rad to
 //                (b_T - 1) rad (any b_T; levels >= 2 exchange rows as before);
-//     bit 1 (x, b_T = 1 only): the box also adds the x halo (HXO cells left/right) and every
-//                thread reads its x neighbours from the staged plane -- at b_T = 1 the threads
-//                then cover only the compute region (kTX x kTY cells): no halo cell is computed,
-//                no shuffle is needed.
+//     bit 1 (x): the box also adds the x halo (HXO cells left/right) and every thread reads its
+//                level-1 x neighbours from the staged plane -- at b_T = 1 the threads then cover
+//                only the compute region (kTX x kTY cells): no halo cell is computed, no shuffle
+//                is needed; at b_T >= 2 levels >= 2 shuffle as before and the threads' x halo
+//                shrinks to (b_T - 1) rad (rounded to vectors: pays for fp64, 2-cell vectors).
 template <typename T, int R, int BT, int VY, int TXT_ = 16, int VX_ = 4, int OS_ = 0>
 struct Kernel3DTraits {
     static constexpr int VX = VX_;
@@ -64,7 +65,7 @@ struct Kernel3DTraits {
     static_assert(OSX || VX >= R, "x halo: a thread's rad neighbour cells must come from one adjacent thread");
     static_assert(!OSX || OSY, "x staging implies y staging");
     static_assert(VX % VecOf<T>::A == 0, "patch rows are whole 16-byte vectors");
-    static_assert(!OSX || BT == 1, "output-stationary x staging is for b_T = 1");
+    static_assert(!OSX || BT == 1 || VX >= R, "x staging at b_T >= 2: levels >= 2 still shuffle");
     static constexpr int kThreads = TXT * TYT;
     static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // thread window, x by y
     static constexpr int HXO = OSX ? ((R + VecOf<T>::A - 1) / VecOf<T>::A) * VecOf<T>::A : 0;  // staged x halo
@@ -440,7 +441,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 };
                 constexpr int XR = BOX ? VY + 2 * R : VY;       // rows needing an x halo
                 T hl[XR][R], hh[XR][R];
-                if constexpr (K::OSX) {
+                if constexpr (K::OSX && L == 1) {
                     // output-stationary (b_T = 1, level 1 = the staged plane): the rad cells left
                     // and right of each row, read from the stage as whole 16-byte vectors
                     constexpr int NVA = K::HXO;          // cells loaded per side (rad rounded to vectors)

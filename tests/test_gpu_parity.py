@@ -229,14 +229,18 @@ def test_output_stationary_bt1(an5d, name, dtype):
     assert not w.any()
 
 
-OY_CASES = [("star3d1r", torch.float32, 4, 256), ("star3d2r", torch.float32, 2, 256), ("box3d1r", torch.float32, 2, 256),
-            ("star3d1r", torch.float64, 3, 512), ("star3d2r", torch.float64, 2, 512), ("box3d1r", torch.float64, 2, 512)]
+OY_CASES = [("star3d1r", torch.float32, 4, 256, False), ("star3d2r", torch.float32, 2, 256, False),
+            ("box3d1r", torch.float32, 2, 256, False), ("star3d1r", torch.float64, 3, 512, False),
+            ("star3d2r", torch.float64, 2, 512, False), ("box3d1r", torch.float64, 2, 512, False),
+            ("star3d1r", torch.float64, 3, 512, True), ("star3d2r", torch.float64, 2, 512, True),
+            ("box3d1r", torch.float64, 2, 512, True)]
 
 
-@pytest.mark.parametrize("name,dtype,bmax,n_thr", OY_CASES)
-def test_y_staged_tiles(an5d, name, dtype, bmax, n_thr):
+@pytest.mark.parametrize("name,dtype,bmax,n_thr,xstage", OY_CASES)
+def test_y_staged_tiles(an5d, name, dtype, bmax, n_thr, xstage):
     """y-staged tiles (kernel3d.cuh OS bit 0): the TMA box adds rad rows above and below, so the
-    threads' y halo shrinks to (b_T - 1) rad.  Bit-identical to the default layout at every b_T,
+    threads' y halo shrinks to (b_T - 1) rad; with x staging (bit 1, fp64 512-thread layout) level 1
+    also reads its x neighbours from the stage.  Bit-identical to the default layout at every b_T,
     within tolerance of the oracle, exact-integer bit-identical, write counts once per sweep."""
     ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
     ext = small_ext(ndim, rad)
@@ -244,14 +248,20 @@ def test_y_staged_tiles(an5d, name, dtype, bmax, n_thr):
     tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
     gx = inputs.global_grid(1234, ext, kind="pm")
     st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    A = 4 if dtype == torch.float32 else 2
+    rup = lambda v: -(-v // A) * A
     for bT in range(1, bmax + 1):
-        cfg = {"bT": bT, "vec": 2, "h": 8, "n_thr": n_thr, "bS": [32 + 2 * rad, 0]}
+        # x staging: loaded width 64 + 2 rup(rad); the logical b_S names it (an5d.h an5d_config)
+        bsx = (64 + 2 * rup(rad) - 2 * rup(bT * rad) + 2 * bT * rad) if xstage else 0
+        cfg = {"bT": bT, "vec": 2, "h": 8, "n_thr": n_thr, "bS": [32 + 2 * rad, bsx]}
         d = st.describe(ext, cfg)
         assert d["bS_loaded"][0] == 32 + 2 * rad and d["compute"][0] == 32 - 2 * (bT - 1) * rad, d
+        if xstage:
+            assert d["bS_loaded"][1] == 64 + 2 * rup(rad), d
         for T in sorted({1, bT, 2 * bT + 3}):
             got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
             ref, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, dict(cfg, bS=[32, 0]))
-            assert np.array_equal(got, ref), (name, bT, T)
+            assert np.array_equal(got, ref), (name, bT, T, xstage)
             exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
             assert ring_equal(got, exp, rad) and rel_linf(got, exp, rad) <= TOL[dtype], (name, bT, T)
         T = _exact_T(ndim, rad, shape, 2 * bT + 3, dtype)
