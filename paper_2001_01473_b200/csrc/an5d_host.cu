@@ -130,29 +130,46 @@ const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0, in
     return best;
 }
 
-// Loaded x width of the tile a configuration names through its logical b_S (0 = not named): the
-// logical halo b_T rad per side rounded up to whole 16-byte vectors (sweep_geometry).
-int cfg_tile_x(const Plan& p, const an5d_config& c) {
-    const int bs = c.bS[p.ndim - 2];
-    if (!bs || !c.bT) return 0;
-    const int A = (int)(16 / p.elem), hl = c.bT * p.rad;
-    return bs - 2 * hl + 2 * ((hl + A - 1) / A) * A;
+// Logical x tile b_S (compute region + 2 b_T rad) of an instance at full degree bT:
+// what a configuration's bS names.  The loaded width minus the loaded halo (whole 16-byte vectors;
+// x-staged 3D layouts: staged vectors + (b_T - 1) rad rounded) plus 2 b_T rad.
+int inst_logical_x(const Plan& p, const Instance& i, int bT) {
+    const int A = (int)(16 / p.elem), R = p.rad;
+    const int hx = (p.ndim == 3 && i.xstage) ? i.xstage + (int)round_up((int64_t)(bT - 1) * R, A)
+                                             : (int)round_up((int64_t)bT * R, A);
+    return i.tile_x_loaded - 2 * hx + 2 * bT * R;
 }
 
-// Loaded y height of a 3D tile a configuration names through b_S_y (0 = not named; 2D: 0).  The y
-// halo is not rounded, so the loaded height is b_S_y itself; it names the cluster layouts (a
-// cluster of CL blocks is one tile of CL x 16 VY rows, NEXT N2).
-int cfg_tile_y(const Plan& p, const an5d_config& c) {
-    return p.ndim == 3 ? c.bS[0] : 0;
+// Does instance i run degree-d sweeps of configuration c's layout?  The layout is named by
+// (vec, direct, threads per block, logical b_S -- x through inst_logical_x at c's b_T, 3D y = the
+// loaded height: the y halo is not rounded) -- fields left 0 match anything.
+bool inst_matches(const Plan& p, const Instance& i, int d, const an5d_config& c, bool any_threads) {
+    if (!(i.ndim == p.ndim && i.shape == p.shape && i.dtype == p.dtype && i.rad == p.rad && i.bT == d &&
+          i.vec == c.vec && i.assoc == (c.direct ? 0 : 1) && std::max(1, i.nf) == p.nf))
+        return false;
+    if (!any_threads && c.n_thr && i.threads != c.n_thr) return false;
+    const int bx = c.bS[p.ndim - 2];
+    if (bx && c.bT && inst_logical_x(p, i, c.bT) != bx) return false;
+    if (p.ndim == 3 && c.bS[0] && i.tile_y != c.bS[0]) return false;
+    return true;
 }
 
 // The instance a sweep of degree d runs under configuration c: the configuration's layout, or for
 // a reduced degree (d < b_T) without that layout (the 2D level split needs d >= 2) the same tile
-// with any thread count -- identical per-cell arithmetic, so the results are the same bits.
+// with any thread count -- identical per-cell arithmetic, so the results are the same bits.  Among
+// several matches the narrowest tile with the fewest threads is the default (the round-1 layouts).
 const Instance* find_instance(const Plan& p, int d, const an5d_config& c) {
-    const Instance* i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), c.n_thr, cfg_tile_y(p, c));
-    if (!i && d < c.bT) i = find_instance(p, d, c.vec, c.direct, cfg_tile_x(p, c), 0, cfg_tile_y(p, c));
-    return i;
+    for (bool any : {false, true}) {
+        if (any && d >= c.bT) break;
+        const Instance* best = nullptr;
+        for (const Instance& i : registry())
+            if (inst_matches(p, i, d, c, any) &&
+                (!best || std::make_tuple(i.tile_x_loaded, i.threads, i.tile_y) <
+                              std::make_tuple(best->tile_x_loaded, best->threads, best->tile_y)))
+                best = &i;
+        if (best) return best;
+    }
+    return nullptr;
 }
 
 int max_bT_for(const Plan& p, int vec) {
@@ -200,7 +217,10 @@ an5d_status sweep_geometry(const Plan& p, const Instance& inst, const Dims& dm, 
         loaded[0] = inst.tile_y;
         halo[0] = d * R;
         loaded[1] = inst.tile_x_loaded;
-        halo[1] = (int)round_up((int64_t)d * R, g.A);
+        // x-staged layouts (kernel3d.cuh OS bit 1): the staged vectors beyond the threads plus the
+        // (d-1) rad the threads' level-1 values shrink by, each rounded to whole vectors
+        halo[1] = inst.xstage ? inst.xstage + (int)round_up((int64_t)(d - 1) * R, g.A)
+                              : (int)round_up((int64_t)d * R, g.A);
     }
     for (int i = 0; i < nb; ++i) {
         g.loaded[i] = loaded[i];
@@ -472,8 +492,9 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
         if (hint && hint->bT && inst.bT != hint->bT) continue;
         if (hint && hint->vec && inst.vec != hint->vec) continue;
         if (hint && hint->n_thr && inst.threads != hint->n_thr) continue;
-        if (hint && cfg_tile_x(p, *hint) && inst.tile_x_loaded != cfg_tile_x(p, *hint)) continue;
-        if (hint && cfg_tile_y(p, *hint) && inst.tile_y != cfg_tile_y(p, *hint)) continue;
+        if (hint && hint->bT && hint->bS[p.ndim - 2] && inst_logical_x(p, inst, hint->bT) != hint->bS[p.ndim - 2])
+            continue;
+        if (hint && p.ndim == 3 && hint->bS[0] && inst.tile_y != hint->bS[0]) continue;
         if (T > 0 && inst.bT > T) continue;
         // every reduced degree the schedule may need must exist with the same tile
         const int ty = p.ndim == 3 ? inst.tile_y : 0;
@@ -507,7 +528,7 @@ std::vector<std::pair<double, an5d_config>> rank_configs(const Plan& p, const Di
             c.vec = inst.vec;
             c.h = h;
             c.n_thr = inst.threads;
-            {   // logical tile b_S = compute region + 2 b_T rad (names the layout, cfg_tile_x)
+            {   // logical tile b_S = compute region + 2 b_T rad (names the layout, inst_matches)
                 SweepGeom g{};
                 sweep_geometry(p, inst, dm, inst.bT, h, 0, dm.E[0], p.rad, dm.E[0] - p.rad, g);
                 for (int i = 0; i < p.ndim - 1; ++i) c.bS[i] = g.C[i] + 2 * inst.bT * p.rad;
@@ -1324,7 +1345,8 @@ an5d_status an5d_tune(an5d_plan* p, const void* grid_in, void* grid_out, const i
         // runs 8-20 % slower; the 512-thread fp64 3D layout runs 15-30 % faster), so every layout
         // is measured rather than ranked.
         auto layout_of = [&](const an5d_config& c) {
-            return std::make_tuple(c.vec, c.n_thr, cfg_tile_x(*p, c), cfg_tile_y(*p, c));
+            const Instance* i = find_instance(*p, c.bT, c);
+            return std::make_tuple(c.vec, c.n_thr, i ? i->tile_x_loaded : 0, i ? i->tile_y : 0);
         };
         std::vector<std::pair<int, int>> pairs;
         for (const auto& r : ranked) {

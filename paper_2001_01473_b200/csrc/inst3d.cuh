@@ -62,6 +62,7 @@ Instance make_instance3d() {
     i.fn_edge = i.fn_interior;
     i.threads = K::kThreads;
     i.tile_x_loaded = K::kTXL;   // loaded width (output-stationary: compute width + 2 x halo)
+    i.xstage = K::HXO;
     i.tile_y = K::kTYL * CL;   // a cluster's blocks form one tile of CL x kTY rows (OS: + 2 rad halo rows)
     i.cluster = CL;
     i.smem_bytes = K::kSmemBytes;

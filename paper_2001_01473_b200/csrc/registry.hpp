@@ -30,6 +30,7 @@ struct Instance {
     size_t smem_bytes;                       // dynamic shared memory per block
     int cluster;                             // 3D: blocks per cluster along y (tile_y = cluster x block rows)
     int nf;                                  // fields advanced together (multi-field systems; 0/1 = one)
+    int xstage;                              // 3D x-staged layouts: staged x halo cells per side (0: none)
 };
 
 std::vector<Instance>& registry();

@@ -251,13 +251,14 @@ def test_y_staged_tiles(an5d, name, dtype, bmax, n_thr, xstage):
     A = 4 if dtype == torch.float32 else 2
     rup = lambda v: -(-v // A) * A
     for bT in range(1, bmax + 1):
-        # x staging: loaded width 64 + 2 rup(rad); the logical b_S names it (an5d.h an5d_config)
-        bsx = (64 + 2 * rup(rad) - 2 * rup(bT * rad) + 2 * bT * rad) if xstage else 0
+        # x staging: loaded width 64 + 2 rup(rad), compute width 64 - 2 rup((b_T - 1) rad); the
+        # logical b_S = compute + 2 b_T rad names the layout (an5d.h an5d_config)
+        bsx = (64 - 2 * rup((bT - 1) * rad) + 2 * bT * rad) if xstage else 0
         cfg = {"bT": bT, "vec": 2, "h": 8, "n_thr": n_thr, "bS": [32 + 2 * rad, bsx]}
         d = st.describe(ext, cfg)
         assert d["bS_loaded"][0] == 32 + 2 * rad and d["compute"][0] == 32 - 2 * (bT - 1) * rad, d
         if xstage:
-            assert d["bS_loaded"][1] == 64 + 2 * rup(rad), d
+            assert d["bS_loaded"][1] == 64 + 2 * rup(rad) and d["compute"][1] == 64 - 2 * rup((bT - 1) * rad), d
         for T in sorted({1, bT, 2 * bT + 3}):
             got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
             ref, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, dict(cfg, bS=[32, 0]))
