@@ -1,7 +1,9 @@
 """Small runs of every kernel family through the C ABI, for compute-sanitizer (racecheck /
 synccheck / memcheck): 2D one warp per tile and the two-warp level split, 3D 256- and 512-thread
 layouts (TMA + mbarrier staging, shared-memory halo exchange), the fp32 box rad-4 runtime plane
-loop, and the fused halo exchange in one process.  Each result is checked against the oracle.
+loop, the fused halo exchange in one process, and (round 2) thread-block clusters, output-
+stationary / staged-halo 3D tiles, gradient2d and a multi-field system.  Each result is checked
+against the oracle.
 
 usage (under gpurun): compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 """
@@ -25,6 +27,14 @@ CASES = [
     ("star3d1r", torch.float32, (13, 40, 140), 7, {"bT": 3, "vec": 2, "h": 4, "n_thr": 256}),
     ("star3d1r", torch.float64, (13, 40, 140), 7, {"bT": 3, "vec": 2, "h": 4, "n_thr": 512}),
     ("box3d4r", torch.float32, (9, 40, 130), 2, {"bT": 1, "vec": 2, "h": 4}),
+    # round 2: clusters (DSMEM halo sharing, split cluster barrier), output-stationary and
+    # y/x-staged tiles, gradient2d, the level split with uniform scheduling
+    ("star3d1r", torch.float32, (13, 80, 140), 7, {"bT": 3, "vec": 2, "h": 4, "n_thr": 256, "bS": [64, 0]}),
+    ("star3d1r", torch.float64, (13, 80, 140), 7, {"bT": 3, "vec": 2, "h": 4, "n_thr": 512, "bS": [64, 0]}),
+    ("box3d3r", torch.float32, (9, 40, 130), 2, {"bT": 1, "vec": 2, "h": 4, "n_thr": 256, "bS": [38, 70]}),
+    ("star3d2r", torch.float32, (13, 40, 140), 5, {"bT": 2, "vec": 2, "h": 4, "n_thr": 256, "bS": [36, 0]}),
+    ("star3d1r", torch.float64, (13, 40, 140), 7, {"bT": 3, "vec": 2, "h": 4, "n_thr": 512, "bS": [34, 66]}),
+    ("gradient2d", torch.float32, (29, 600), 7, {"bT": 3, "vec": 8, "h": 8}),
 ]
 
 
@@ -48,6 +58,19 @@ def main():
         err = rel(b.cpu().numpy(), oracle.run(g, rad, shape, tab, div, T, npdt), rad)
         print(f"{name} {dt} {cfg}: rel_linf {err:.2e}", flush=True)
         assert err <= (1e-5 if dt == torch.float32 else 1e-12)
+    # multi-field system (2 fields, one kernel)
+    ndim, rad, shape, nf, tab = inputs.system_problem("star2d1r-x2")
+    ext = (31, 602)
+    f = inputs.system_fields(5, nf, ext)
+    sy = an5d.System(ndim, rad, shape, tab, torch.float32)
+    a = an5d.to_fields(torch.from_numpy(f.astype(np.float32)).cuda(), rad)
+    b = an5d.empty_fields(nf, ext, rad, torch.float32)
+    sy.run(a, b, 9, {"bT": 3, "vec": 8, "h": 8})
+    torch.cuda.synchronize()
+    exp = oracle.run_system(f, rad, shape, tab, 9, np.float32)
+    err = float(np.abs(b.cpu().numpy() - exp).max() / np.abs(exp).max())
+    print(f"star2d1r-x2 float32: rel_linf {err:.2e}", flush=True)
+    assert err <= 1e-5
     # fused halo exchange, 3 slabs on one device
     ndim, rad, shape, tab, div = inputs.benchmark_problem("star2d1r")
     gext = (62 + 2 * rad, 300 + 2 * rad)
