@@ -1,5 +1,5 @@
 """Run N sweeps of one 2D/3D stencil configuration (for ncu captures):
-sweeponly.py name dtype bT h vec n [n_thr]."""
+sweeponly.py name dtype bT h vec n [n_thr [bS_y]]  (3D bS_y: the loaded tile height naming a layout)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -12,7 +12,10 @@ size = 16384 if ndim == 2 else 512
 ext = (size + 2 * rad,) * ndim
 st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
 nthr = int(sys.argv[7]) if len(sys.argv) > 7 else 0
-cfg = st.plan_config(ext, 1000, {"bT": bt, "h": h, "vec": vec, "n_thr": nthr})
+hint = {"bT": bt, "h": h, "vec": vec, "n_thr": nthr}
+if len(sys.argv) > 8:
+    hint["bS"] = [int(sys.argv[8]), 0]
+cfg = st.plan_config(ext, 1000, hint)
 print(cfg, file=sys.stderr)
 a = an5d.empty_grid(ext, rad, dtype); b = an5d.empty_grid(ext, rad, dtype)
 fill_uniform(a, 1, ext); b.copy_(a)
