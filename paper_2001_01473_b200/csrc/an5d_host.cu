@@ -133,11 +133,22 @@ const Instance* find_instance(const Plan& p, int bT, int vec, int direct = 0, in
 // Logical x tile b_S (compute region + 2 b_T rad) of an instance at full degree bT:
 // what a configuration's bS names.  The loaded width minus the loaded halo (whole 16-byte vectors;
 // x-staged 3D layouts: staged vectors + (b_T - 1) rad rounded) plus 2 b_T rad.
-int inst_logical_x(const Plan& p, const Instance& i, int bT) {
+// 3D layouts without x staging hold a loaded x halo of exactly d rad (not rounded to a 16-byte
+// vector) when fp32 and d rad = 2 mod 4 (kernel3d.cuh Kernel3DTraits::XPAIR; the instance of
+// degree d carries the same decision in Instance::xpair, checked in sweep_geometry).
+bool xpair_rule(const Plan& p, const Instance& i, int d) {
+    return p.ndim == 3 && !i.xstage && p.elem == 4 && (d * p.rad) % 4 == 2;
+}
+
+// loaded x halo of instance i's layout at degree d
+int x_halo(const Plan& p, const Instance& i, int d) {
     const int A = (int)(16 / p.elem), R = p.rad;
-    const int hx = (p.ndim == 3 && i.xstage) ? i.xstage + (int)round_up((int64_t)(bT - 1) * R, A)
-                                             : (int)round_up((int64_t)bT * R, A);
-    return i.tile_x_loaded - 2 * hx + 2 * bT * R;
+    if (p.ndim == 3 && i.xstage) return i.xstage + (int)round_up((int64_t)(d - 1) * R, A);
+    return xpair_rule(p, i, d) ? d * R : (int)round_up((int64_t)d * R, A);
+}
+
+int inst_logical_x(const Plan& p, const Instance& i, int bT) {
+    return i.tile_x_loaded - 2 * x_halo(p, i, bT) + 2 * bT * p.rad;
 }
 
 // Does instance i run degree-d sweeps of configuration c's layout?  The layout is named by
@@ -219,8 +230,10 @@ an5d_status sweep_geometry(const Plan& p, const Instance& inst, const Dims& dm, 
         loaded[1] = inst.tile_x_loaded;
         // x-staged layouts (kernel3d.cuh OS bit 1): the staged vectors beyond the threads plus the
         // (d-1) rad the threads' level-1 values shrink by, each rounded to whole vectors
-        halo[1] = inst.xstage ? inst.xstage + (int)round_up((int64_t)(d - 1) * R, g.A)
-                              : (int)round_up((int64_t)d * R, g.A);
+        // (XPAIR layouts: exactly d rad; the host rule and the compiled instance must agree)
+        if (xpair_rule(p, inst, d) != (inst.xpair != 0))
+            return fail(AN5D_ERR_UNSUPPORTED, "instance x-halo rule mismatch (degree %d)", d);
+        halo[1] = x_halo(p, inst, d);
     }
     for (int i = 0; i < nb; ++i) {
         g.loaded[i] = loaded[i];
@@ -661,7 +674,8 @@ an5d_status encode_tmap_3d(const Plan& p, const Instance& inst, const void* src,
     // one block's plane: a cluster layout's blocks each load their own tile_y / cluster rows
     // (a cluster layout's block also stages rad pad rows above and below: kernel3d.cuh kBoxRows)
     const int cl = std::max(1, inst.cluster);
-    const cuuint32_t box[3] = {(cuuint32_t)inst.tile_x_loaded,
+    // (XPAIR: the box starts 2 cells before the window and is 4 cells wider, kernel3d.cuh kTXL)
+    const cuuint32_t box[3] = {(cuuint32_t)(inst.tile_x_loaded + (inst.xpair ? 4 : 0)),
                                (cuuint32_t)(inst.tile_y / cl + (cl > 1 ? 2 * p.rad : 0)), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(&tm, p.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,

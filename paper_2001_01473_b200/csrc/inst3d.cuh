@@ -25,17 +25,17 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
     auto fn = &an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL, OS>;
     static bool attr_set = false;   // once per instance (a per-launch attribute call costs host time)
     if (!attr_set) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::kSmemBytes);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem_total(CL));
         attr_set = true;
     }
     if constexpr (CL == 1) {
-        fn<<<(unsigned)blocks, K::kThreads, K::kSmemBytes, st>>>(a, cf, tmap);
+        fn<<<(unsigned)blocks, K::kThreads, K::smem_total(CL), st>>>(a, cf, tmap);
     } else {
         // one cluster of CL blocks per unit (NEXT N2: cluster halo sharing along y)
         cudaLaunchConfig_t lc{};
         lc.gridDim = dim3((unsigned)(blocks * CL), 1, 1);
         lc.blockDim = dim3(K::kThreads, 1, 1);
-        lc.dynamicSmemBytes = K::kSmemBytes;
+        lc.dynamicSmemBytes = K::smem_total(CL);
         lc.stream = st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -61,11 +61,12 @@ Instance make_instance3d() {
     i.fn_interior = reinterpret_cast<const void*>(&an5d_sweep3d<T, R, BT, VY, BOX, TXT, VX, CL, OS>);
     i.fn_edge = i.fn_interior;
     i.threads = K::kThreads;
-    i.tile_x_loaded = K::kTXL;   // loaded width (output-stationary: compute width + 2 x halo)
+    i.tile_x_loaded = K::kTXW;   // loaded window (output-stationary: compute width + 2 x halo)
+    i.xpair = K::XPAIR ? 1 : 0;  // x halo b_T rad exactly; TMA box 2 XOFF cells wider (Kernel3DTraits)
     i.xstage = K::HXO;
     i.tile_y = K::kTYL * CL;   // a cluster's blocks form one tile of CL x kTY rows (OS: + 2 rad halo rows)
     i.cluster = CL;
-    i.smem_bytes = K::kSmemBytes;
+    i.smem_bytes = K::smem_total(CL);
     return i;
 }
 

@@ -69,7 +69,19 @@ struct Kernel3DTraits {
     static constexpr int kThreads = TXT * TYT;
     static constexpr int kTX = TXT * VX, kTY = TYT * VY;    // thread window, x by y
     static constexpr int HXO = OSX ? ((R + VecOf<T>::A - 1) / VecOf<T>::A) * VecOf<T>::A : 0;  // staged x halo
-    static constexpr int kTXL = kTX + 2 * HXO;              // loaded / staged row (= kTX unless OS)
+    // XPAIR (fp32, no x staging, b_T rad = 2 mod 4): the loaded x halo is b_T rad itself instead of
+    // b_T rad rounded up to a 16-byte vector, so the compute width is kTX - 2 b_T rad (b_T 2, rad 1:
+    // 60 instead of 56 -- at 512^3 9 x tiles instead of 10).  A TMA box must start on a 16-byte x
+    // boundary (an unaligned start faults: profiles/r02z_xpair_probe_unaligned_tma.txt), so the box
+    // starts XOFF = 2 cells before the window and is 4 cells wider; threads read their patch XOFF
+    // cells into the staged row (8-byte shared loads) and store 8-byte cell pairs (every patch and
+    // every compute region then starts 2 cells off a 16-byte boundary; the compute width is a
+    // multiple of 4).  Other halos keep the rounding.
+    static constexpr bool XPAIR = sizeof(T) == 4 && HXO == 0 && (BT * R) % 4 == 2;
+    static constexpr int XOFF = XPAIR ? 2 : 0;              // staged column of the window's first cell
+    static constexpr int SG = XPAIR ? 2 : VecOf<T>::A;       // store granule (cells)
+    static constexpr int kTXW = kTX + 2 * HXO;              // loaded window (cells)
+    static constexpr int kTXL = kTXW + 2 * XOFF;            // staged row = TMA box width (= kTX unless OS / XPAIR)
     static constexpr int kTYL = kTY + (OSY ? 2 * R : 0);    // loaded rows
     static constexpr int PROWS = kTY + 2 * R;               // staged rows (R pad rows per side; OS: halo rows)
     // elements per staged plane, rounded to 128 bytes: every slot is a TMA destination, which must
@@ -102,6 +114,14 @@ struct Kernel3DTraits {
     static constexpr int D = SK ? D1 : D0;                  // staged planes
     static constexpr int NXB = SK ? 2 * (BT - 1) : 2;       // exchange buffers
     static constexpr size_t kSmemBytes = smem_of(D, NXB);
+    // XPAIR rows are kTXL = kTX + 4 cells, so a layout whose TMA box lands R rows into the slot
+    // (no cluster, no y staging) would put the box off the 128-byte boundary TMA destinations need
+    // (misaligned address): the whole shared-memory layout then starts LEAD cells late, with
+    // LEAD + R kTXL = 0 mod 32 cells (slots stay multiples of 128 bytes)
+    static constexpr int lead(int cl) {
+        return (XPAIR && !(cl > 1 || OSY)) ? (32 - (R * kTXL) % 32) % 32 : 0;
+    }
+    static constexpr size_t smem_total(int cl) { return kSmemBytes + (size_t)lead(cl) * sizeof(T); }
 };
 
 // unit -> (tile y, tile x, stream block): frame tiles (those that can touch the ring or the array
@@ -221,17 +241,20 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     T* const stage = smem;                              // D planes of PROWS x kTX
     T* const xch = smem + (size_t)D * K::PLANE;         // 2 exchange buffers
     const int own = (ys + R) * kTX + xs;                // patch origin inside a staged plane
+    const int own_st = own + K::XOFF;                   // ... of the staged (TMA) plane itself (XPAIR)
 
-    // per-thread masks (EDGE): ring cells, store coverage
+    // per-thread masks (EDGE): ring cells, store coverage (st_full: whole store granules of SG
+    // cells -- 16-byte vectors, or 8-byte pairs for XPAIR tiles)
+    constexpr int SG = K::SG, NSG = VX / SG;
     unsigned ring_mask = 0, st_full = 0, st_elem = 0;
 #pragma unroll
     for (int yy = 0; yy < VY; ++yy) {
         const int y = gy0 + yy;
         const bool yin = y >= 0 && y < a.Ey;
 #pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-            const int x = gx0 + j * A;
-            if (y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x + A <= g.cx1) st_full |= 1u << (yy * NCH + j);
+        for (int j = 0; j < NSG; ++j) {
+            const int x = gx0 + j * SG;
+            if (y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x + SG <= g.cx1) st_full |= 1u << (yy * NSG + j);
         }
         if constexpr (EDGE) {
 #pragma unroll
@@ -240,7 +263,7 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 const bool in = yin && x >= 0 && x < a.Ex;
                 const bool ring = y < R || y >= a.Ey - R || x < R || x >= a.Ex - R;
                 if (in && ring) ring_mask |= 1u << (yy * VX + xx);
-                if (!((st_full >> (yy * NCH + xx / A)) & 1u) && y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x < g.cx1)
+                if (!((st_full >> (yy * NSG + xx / SG)) & 1u) && y >= g.cy0 && y < g.cy1 && x >= g.cx0 && x < g.cx1)
                     st_elem |= 1u << (yy * VX + xx);
             }
         }
@@ -257,7 +280,8 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
         if (tid == 0) {
             if (q >= g.s_a && q < g.s_b) {
                 mbar_arrive_expect_tx(mbar + slot, kBoxBytes);
-                tma_load_3d(stage + (size_t)slot * K::PLANE + ((CL > 1 || K::OSY) ? 0 : R * kTX), tmap, g.wx0 + a.x_off,
+                tma_load_3d(stage + (size_t)slot * K::PLANE + ((CL > 1 || K::OSY) ? 0 : R * kTX), tmap,
+                            g.wx0 - K::XOFF + a.x_off,
                             g.wy0 - (CL > 1 ? R : 0), (int)q, mbar + slot);
             } else {
                 mbar_arrive(mbar + slot);
@@ -275,6 +299,21 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
 #pragma unroll
         for (int j = 0; j < NCH; ++j) ld_vec_shared<T>(c + j * A, p + j * A);
         LN::from_cells(P_, c);
+    };
+    // a patch row of a STAGED plane: XPAIR rows are 8-byte (not 16-byte) aligned
+    auto load_row_st = [&](E (&P_)[NE], const T* p) {
+        if constexpr (K::XPAIR) {
+            T c[VX];
+#pragma unroll
+            for (int j = 0; j < VX; j += 2) {
+                const float2 v = *reinterpret_cast<const float2*>(p + j);
+                c[j] = v.x;
+                c[j + 1] = v.y;
+            }
+            LN::from_cells(P_, c);
+        } else {
+            load_row(P_, p);
+        }
     };
     auto store_row = [&](T* p, const E (&P_)[NE]) {
         T c[VX];
@@ -317,15 +356,15 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
     // pin plane qi (relative index) of a patch to its original ring values, read from the stage
     auto pin = [&](E (&u)[VY][NE], int qi) {
         if (qi < ra || qi >= rb) return;                  // not in the array: feeds nothing kept
-        const T* sq = stage + (size_t)(qi % D) * K::PLANE + own;
+        const T* sq = stage + (size_t)(qi % D) * K::PLANE + own_st;
         if (qi < rlo || qi >= rhi) {                      // z-ring plane: every cell
 #pragma unroll
-            for (int yy = 0; yy < VY; ++yy) load_row(u[yy], sq + yy * kTX);
+            for (int yy = 0; yy < VY; ++yy) load_row_st(u[yy], sq + yy * kTX);
         } else if (EDGE && g.ring_xy && ring_mask) {      // x/y-ring cells of this thread
 #pragma unroll
             for (int yy = 0; yy < VY; ++yy) {
                 E o[NE];
-                load_row(o, sq + yy * kTX);
+                load_row_st(o, sq + yy * kTX);
 #pragma unroll
                 for (int xx = 0; xx < VX; ++xx) {
                     T& uc = LN::cell(u[yy], xx);
@@ -409,11 +448,11 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                 E yh_lo[R][NE], yh_hi[R][NE];
                 if constexpr (L == 1) {
 #pragma unroll
-                    for (int yy = 0; yy < VY; ++yy) load_row(u0[yy], cur + own + yy * kTX);
+                    for (int yy = 0; yy < VY; ++yy) load_row_st(u0[yy], cur + own_st + yy * kTX);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {   // (clusters: the staged pad rows are real rows)
-                        load_row(yh_lo[r], cur + own + (r - R) * kTX);
-                        load_row(yh_hi[r], cur + own + (VY + r) * kTX);
+                        load_row_st(yh_lo[r], cur + own_st + (r - R) * kTX);
+                        load_row_st(yh_hi[r], cur + own_st + (VY + r) * kTX);
                     }
                 } else if constexpr (SK) {
                     // halo rows of level L-1's plane of the previous step, exchanged at its end
@@ -648,12 +687,17 @@ __device__ __forceinline__ void sweep3d_unit(const Sweep3DArgs& a, const Coeffs3
                         T c[VX];
                         LN::to_cells(c, fin[yy]);
 #pragma unroll
-                        for (int j = 0; j < NCH; ++j) {
-                            if ((st_full >> (yy * NCH + j)) & 1u) st_vec_global<T>(op + yy * a.py + j * A, c + j * A);
+                        for (int j = 0; j < NSG; ++j) {
+                            if ((st_full >> (yy * NSG + j)) & 1u) {
+                                if constexpr (K::XPAIR)
+                                    *reinterpret_cast<float2*>(op + yy * a.py + j * SG) = make_float2(c[j * SG], c[j * SG + 1]);
+                                else
+                                    st_vec_global<T>(op + yy * a.py + j * SG, c + j * SG);
+                            }
                             if constexpr (EDGE) {
 #pragma unroll
-                                for (int e = 0; e < A; ++e)
-                                    if ((st_elem >> (yy * VX + j * A + e)) & 1u) op[yy * a.py + j * A + e] = c[j * A + e];
+                                for (int e = 0; e < SG; ++e)
+                                    if ((st_elem >> (yy * VX + j * SG + e)) & 1u) op[yy * a.py + j * SG + e] = c[j * SG + e];
                             }
                         }
                     }
@@ -734,7 +778,7 @@ __global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
 an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* const smem = reinterpret_cast<T*>(smem_raw);
+    T* const smem = reinterpret_cast<T*>(smem_raw) + K::lead(CL);
     const int64_t unit = blockIdx.x / CL;
     const unsigned crank = CL > 1 ? cluster_ctarank() : 0;
     if (unit >= a.n_units) return;   // the whole cluster (same unit) leaves together
@@ -768,7 +812,7 @@ an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, con
     g.s_end = g.p1 + (int64_t)BT * R;
     g.s_a = max(g.s_first, (int64_t)0);
     g.s_b = min(g.s_end, a.Ez);
-    g.ring_xy = g.wy0 < R || g.wy0 + K::kTYL > a.Ey - R || g.wx0 < R || g.wx0 + K::kTXL > a.Ex - R;
+    g.ring_xy = g.wy0 < R || g.wy0 + K::kTYL > a.Ey - R || g.wx0 < R || g.wx0 + K::kTXW > a.Ex - R;
     // z-ring planes and the array's z ends are handled by both variants (uniform per-step checks);
     // the EDGE variant is only for tiles whose window touches the x/y ring or the array end
     if (threadIdx.x == 0) tma_prefetch_desc(&tmap);

@@ -31,6 +31,7 @@ struct Instance {
     int cluster;                             // 3D: blocks per cluster along y (tile_y = cluster x block rows)
     int nf;                                  // fields advanced together (multi-field systems; 0/1 = one)
     int xstage;                              // 3D x-staged layouts: staged x halo cells per side (0: none)
+    int xpair;                               // 3D: loaded x halo = b_T rad exactly (Kernel3DTraits::XPAIR)
 };
 
 std::vector<Instance>& registry();

@@ -283,6 +283,52 @@ def test_y_staged_tiles(an5d, name, dtype, bmax, n_thr, xstage):
         assert not w.any(), bT
 
 
+# x-pair 3D tiles (kernel3d.cuh Kernel3DTraits::XPAIR): fp32 layouts without x staging whose
+# b_T rad = 2 mod 4 load an x halo of exactly b_T rad (the TMA box starts on the 16-byte boundary
+# 2 cells before the window and is 4 cells wider) and store 8-byte cell pairs; (stencil, b_T,
+# loaded tile height bS_y naming the layout: 32 default, 32 + 2 rad y-staged, 64 cluster pair)
+XPAIR_CASES = [("star3d1r", 2, 32), ("star3d1r", 2, 34), ("star3d1r", 2, 64), ("box3d1r", 2, 32),
+               ("box3d1r", 2, 34), ("j3d27pt", 2, 64), ("star3d2r", 1, 32), ("box3d2r", 1, 32)]
+
+
+@pytest.mark.parametrize("name,bT,bsy", XPAIR_CASES)
+def test_xpair_tiles(an5d, name, bT, bsy):
+    """Geometry (bit-exact): loaded x halo b_T rad, compute width 64 - 2 b_T rad, tile count
+    ceil(I_x / C_x); exact-integer GPU == oracle bit for bit; random inputs within
+    tolerance; every interior cell stored exactly once per sweep (ragged grid, several x tiles,
+    compute regions 2 cells off a 16-byte boundary)."""
+    dtype = torch.float32
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    ext = small_ext(ndim, rad)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    cfg = {"bT": bT, "vec": 2, "h": 8, "n_thr": 256, "bS": [bsy, 0]}
+    d = st.describe(ext, cfg)
+    assert (bT * rad) % 4 == 2
+    assert d["halo_loaded"][1] == bT * rad and d["compute"][1] == 64 - 2 * bT * rad, d
+    assert d["n_tiles"][1] == -(-(ext[2] - 2 * rad) // (64 - 2 * bT * rad)), d
+    g = inputs.global_grid(inputs.DEFAULT_SEED, ext)
+    for T in sorted({bT, 2 * bT + 1}):
+        got, _ = gpu_run(an5d, ndim, rad, shape, tab, div, g, T, dtype, cfg)
+        exp = oracle.run(g, rad, shape, tab, div, T, NP[dtype])
+        assert ring_equal(got, exp, rad) and rel_linf(got, exp, rad) <= TOL[dtype], (name, bT, bsy, T)
+    tabx, divx = inputs.coeff_table(ndim, rad, shape, seed=99, kind="pm1")
+    gx = inputs.global_grid(1234, ext, kind="pm")
+    T = _exact_T(ndim, rad, shape, 2 * bT + 3, dtype)
+    got, _ = gpu_run(an5d, ndim, rad, shape, tabx, divx, gx, T, dtype, cfg)
+    assert np.array_equal(got, oracle.run(gx, rad, shape, tabx, divx, T, NP[dtype])), (name, bT, bsy, T)
+    a = an5d.to_grid(torch.from_numpy(g.astype(NP[dtype])).cuda(), rad)
+    b = an5d.empty_grid(ext, rad, dtype)
+    wc = torch.zeros(ext, dtype=torch.int32, device="cuda")
+    st.copy_ring(a, b)
+    st.sweep(a, b, bT, cfg, write_count=wc)
+    torch.cuda.synchronize()
+    w = wc.cpu().numpy()
+    core = tuple(slice(rad, e - rad) for e in ext)
+    assert np.all(w[core] == 1), (name, bT, bsy)
+    w[core] = 0
+    assert not w.any(), (name, bT, bsy)
+
+
 CLUSTER_CASES = [("star3d1r", torch.float32, 4, 256, (2, 4)), ("star3d2r", torch.float32, 2, 256, (2,)),
                  ("box3d1r", torch.float32, 2, 256, (2,)), ("j3d27pt", torch.float32, 2, 256, (2,)),
                  ("star3d1r", torch.float64, 3, 256, (2,)), ("star3d1r", torch.float64, 3, 512, (2,)),
