@@ -2,6 +2,7 @@
 // Product code: never includes or links anything from oracle/.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <type_traits>
 
@@ -102,6 +103,25 @@ __device__ __forceinline__ void cp_async_elem_pred(void* sdst, const void* gsrc,
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---- programmatic dependent launch (PDL) between consecutive sweeps ------------------------------
+// A sweep launched with cudaLaunchAttributeProgrammaticStreamSerialization may be scheduled while
+// the previous sweep on the stream is still draining its last units; every sweep kernel therefore
+// starts with pdl_wait() (griddepcontrol.wait: blocks until the previous grid has COMPLETED and its
+// memory is visible -- before any global read or write, so the in-place buffer reuse of the sweep
+// schedule stays ordered) and then pdl_trigger() (lets the NEXT sweep's blocks be scheduled onto
+// SMs this grid frees).  Trigger after wait, never before: a grid two launches ahead holding SM
+// slots while this one still needs them could deadlock.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+// host: PDL on unless AN5D_PDL=0 (A/B switch, read once)
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("AN5D_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 // ---- TMA (cp.async.bulk.tensor) + mbarrier: whole tile planes staged by one thread ---------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {

@@ -35,8 +35,19 @@ cudaError_t launch2d(const Sweep2DArgs& a, const void* coeffs, int64_t blocks, b
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    fn<<<(unsigned)blocks, 32 * NW, smem, st>>>(a, cf);
-    return cudaGetLastError();
+    // programmatic dependent launch (common.cuh PDL): the kernel waits for the previous grid itself
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)blocks, 1, 1);
+    lc.blockDim = dim3(32 * NW, 1, 1);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&lc, fn, a, cf);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T, int R, int BT, int V, bool BOX, bool ASSOC = true, int NW = 1, bool GRAD = false, int NF = 1>

@@ -28,25 +28,31 @@ cudaError_t launch3d(const Sweep3DArgs& a, const void* coeffs, const CUtensorMap
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem_total(CL));
         attr_set = true;
     }
-    if constexpr (CL == 1) {
-        fn<<<(unsigned)blocks, K::kThreads, K::smem_total(CL), st>>>(a, cf, tmap);
-    } else {
-        // one cluster of CL blocks per unit (NEXT N2: cluster halo sharing along y)
-        cudaLaunchConfig_t lc{};
-        lc.gridDim = dim3((unsigned)(blocks * CL), 1, 1);
-        lc.blockDim = dim3(K::kThreads, 1, 1);
-        lc.dynamicSmemBytes = K::smem_total(CL);
-        lc.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = CL;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        lc.attrs = at;
-        lc.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&lc, fn, a, cf, tmap);
-        if (e != cudaSuccess) return e;
+    // one cluster of CL blocks per unit (NEXT N2: cluster halo sharing along y); programmatic
+    // dependent launch (common.cuh PDL): the kernel waits for the previous grid itself
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)(blocks * CL), 1, 1);
+    lc.blockDim = dim3(K::kThreads, 1, 1);
+    lc.dynamicSmemBytes = K::smem_total(CL);
+    lc.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
     }
+    if constexpr (CL > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = CL;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    lc.attrs = at;
+    lc.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&lc, fn, a, cf, tmap);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

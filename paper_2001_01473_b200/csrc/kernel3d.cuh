@@ -777,6 +777,8 @@ template <typename T, int R, int BT, int VY, bool BOX, int TXT = 16, int VX = 4,
 __global__ void __launch_bounds__(TXT * 16, min_blocks_3d<T, VY, R, BOX, TXT>())
 an5d_sweep3d(const Sweep3DArgs a, const __grid_constant__ Coeffs3D<T, R> cf, const __grid_constant__ CUtensorMap tmap) {
     using K = Kernel3DTraits<T, R, BT, VY, TXT, VX, OS>;
+    pdl_wait();      // the previous sweep has completed (common.cuh PDL)
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* const smem = reinterpret_cast<T*>(smem_raw) + K::lead(CL);
     const int64_t unit = blockIdx.x / CL;
