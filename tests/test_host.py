@@ -291,3 +291,34 @@ def test_run_table_unit_count(an5d, monkeypatch):
     monkeypatch.setenv("AN5D_RUN_FRAC", "0")
     g4 = s3.describe([514] * 3, {"bT": 2, "h": 16, "vec": 2})
     assert g4["n_units"] == g4["n_tb_prime"] == g3["n_tb_prime"]
+
+
+@pytest.mark.parametrize("name", ["star3d1r", "star3d2r", "box3d1r", "box3d2r", "j3d27pt"])
+@pytest.mark.parametrize("dtype_name", ["float32", "float64"])
+def test_3d_x_halo_rule(name, dtype_name, an5d):
+    """Loaded x halo of the 3D layouts without x staging (x-pair tiles): fp32 with
+    b_T rad = 2 (mod 4) loads exactly b_T rad (compute width 64 - 2 b_T rad); every other case
+    rounds b_T rad up to a 16-byte vector (4 fp32 / 2 fp64 cells).  The compute region and tile
+    count then follow P:320 / P:323 from the logical b_S the library reports."""
+    import torch
+
+    import inputs
+    ndim, rad, shape, tab, div = inputs.benchmark_problem(name)
+    dtype = getattr(torch, dtype_name)
+    st = an5d.Stencil(ndim, rad, shape, tab, div, dtype)
+    ext = [512 + 2 * rad] * 3
+    A = 4 if dtype == torch.float32 else 2
+    n = 0
+    for bT in range(1, 7):
+        try:
+            g = st.describe(ext, {"bT": bT, "vec": 2, "h": 64, "n_thr": 256, "bS": [32, 0]})
+        except an5d.AN5DError as e:
+            assert e.status in (2, 5)
+            continue
+        n += 1
+        hr = bT * rad
+        want = hr if (A == 4 and hr % 4 == 2) else -(-hr // A) * A
+        assert g["bS_loaded"][1] == 64 and g["halo_loaded"][1] == want, (bT, g)
+        assert g["compute"][1] == 64 - 2 * want == og.compute_region(g["bS"][1], bT, rad), (bT, g)
+        assert g["n_tiles"][1] == math.ceil(512 / g["compute"][1]), (bT, g)
+    assert n > 0
