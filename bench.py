@@ -272,6 +272,8 @@ def main():
                          "send/recv from Python (nccl) or the library's own NCCL communicator (lib, an5d_set_comm)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="single GPU: time CUDA-graph replays of the captured T-step run (one graph per buffer parity)")
     ap.add_argument("--ref-step-seconds", type=float, default=3.0)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--T", type=int, default=0, help="override the time-step count")
@@ -374,6 +376,23 @@ def run_an5d(args):
         step(i)
     torch.cuda.synchronize()
     launches_per_step = st.last_launch_count()
+    if args.graph:
+        # the whole T-step run (ring copy + every sweep) captured once per buffer parity as a CUDA
+        # graph after the eager warm-up (run tables and occupancy are cached by then), replayed
+        graphs = []
+        for par in (0, 1):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                st.run(bufs[par], bufs[1 - par], T, cfg)
+            graphs.append(gph)
+        torch.cuda.synchronize()
+
+        def step(i):
+            graphs[i % 2].replay()
+
+        for i in range(2):
+            step(args.warmup + i)
+        torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local) as clk:
         torch.cuda.synchronize()
@@ -519,7 +538,8 @@ def run_an5d(args):
                    "planner": "model" if args.no_tune else "model top-5, measured pick (P:784-793)",
                    "bS": geom["bS"][:nb], "bS_loaded": geom["bS_loaded"][:nb],
                    "parallelism": "1 GPU", "l2": f"inputs larger than L2 ({a.numel() * a.element_size() / 2**30:.2f} GiB per grid buffer > 126 MB)",
-                   "regs_per_thread": geom["regs_per_thread"]},
+                   "regs_per_thread": geom["regs_per_thread"],
+                   "launch": "cuda_graph" if args.graph else "stream"},
         "gflops": round(gcells * F, 2),
         "roofline": rl,
         "cpu_baseline": cpu,
