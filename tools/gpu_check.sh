@@ -9,6 +9,10 @@
 #   suite      bench --suite "$SUITE" (default all,config4) one line per workload
 #   fmaform    FMA-pipe operand-form microbenchmark (tools/fmaform.cu)
 #   ab         A/B: bench $AB_ARGS with the default lib and with AN5D_LIB=$AB_LIB, $AB_REPS times
+#   absuite    A/B: bench --suite $SUITE with the default lib and with AN5D_LIB=$AB_LIB, $AB_REPS times
+#   abenv      A/B: bench $AB_ARGS with and without the environment setting $AB_ENV (e.g. AN5D_PDL=0)
+#   graph      CUDA-graph bit-identity tests + bench with and without --graph, $AB_REPS times
+#   probe      tools/xpair_probe.py (each 3D x-pair case in its own process)
 TAG=${1:-run}; shift
 mkdir -p gpurun_out
 for what in "$@"; do
@@ -42,5 +46,23 @@ for what in "$@"; do
         python bench.py --no-cpu-baseline --no-e2e ${AB_ARGS} >> gpurun_out/${TAG}_ab_default.jsonl 2>> gpurun_out/${TAG}_ab.err
         AN5D_LIB=$PWD/${AB_LIB} python bench.py --no-cpu-baseline --no-e2e ${AB_ARGS} >> gpurun_out/${TAG}_ab_variant.jsonl 2>> gpurun_out/${TAG}_ab.err
       done ;;
+    absuite)
+      for rep in $(seq ${AB_REPS:-2}); do
+        python bench.py --suite ${SUITE:-all} --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_suite_default.jsonl 2>> gpurun_out/${TAG}_ab.err
+        AN5D_LIB=$PWD/${AB_LIB} python bench.py --suite ${SUITE:-all} --steps 2 --warmup 1 --no-cpu-baseline --no-e2e >> gpurun_out/${TAG}_suite_variant.jsonl 2>> gpurun_out/${TAG}_ab.err
+      done ;;
+    abenv)
+      for rep in $(seq ${AB_REPS:-3}); do
+        python bench.py --no-cpu-baseline --no-e2e ${AB_ARGS} >> gpurun_out/${TAG}_ab_default.jsonl 2>> gpurun_out/${TAG}_ab.err
+        env ${AB_ENV} python bench.py --no-cpu-baseline --no-e2e ${AB_ARGS} >> gpurun_out/${TAG}_ab_variant.jsonl 2>> gpurun_out/${TAG}_ab.err
+      done ;;
+    graph)
+      python -m pytest tests -m gpu -q -k cuda_graph > gpurun_out/${TAG}_pytest_graph.txt 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_pytest_graph.txt
+      for rep in $(seq ${AB_REPS:-2}); do
+        python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-tune --bt 8 --h 45 --graph >> gpurun_out/${TAG}_ab_graph.jsonl 2>> gpurun_out/${TAG}_ab.err
+        python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-tune --bt 8 --h 45 >> gpurun_out/${TAG}_ab_stream.jsonl 2>> gpurun_out/${TAG}_ab.err
+      done ;;
+    probe)
+      python tools/xpair_probe.py > gpurun_out/${TAG}_probe.txt 2>&1 ;;
   esac
 done
